@@ -1,0 +1,364 @@
+"""Benchmark of the B200 SIPG-Laplacian apply (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+                    [--config c4|c3|c5|c5f32|c1|c2] [--cells n]
+
+One step = one y = A u over the whole mesh (all ranks). Default workload:
+BASELINE.json configs[3] ("C4"): 3D SIPG Laplacian, deformed 128^3-cell hex
+mesh (vertex bump x + 0.1 h sin 2pi x sin 2pi y sin 2pi z), p = 5, variable
+coefficient a(x) = 1 + 0.5 sin(pi x) cos(pi y) at the quadrature points,
+fp64, 452,984,832 DoFs; u ~ U[-1,1] from seed 3 (std::mt19937 convention).
+Cells are split in contiguous lexicographic slabs over N GPUs (strong
+scaling) with NCCL ghost exchange overlapped with interior cells.
+
+Rank 0 prints ONE JSON line. Timing: W warm-up steps, then K steps
+bracketed by barrier + cudaDeviceSynchronize, CUDA events on the launching
+stream, max over ranks. Inputs (u 3.6 GB + geometry ~49 GB) exceed the
+126 MB L2, so no flush is needed between steps.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    # name: (d, cells, p, periodic, geometry kind, coefficient, precision, seed, label)
+    "c4": (3, 128, 5, False, "vertex", True, "fp64", 3,
+           "C4: 3D SIPG, deformed 128^3, p=5, a(x) folded, fp64"),
+    "c3": (3, 64, 4, False, "vertex", False, "fp64", 2,
+           "C3: 3D SIPG, deformed 64^3, p=4, per-q J^-T and JxW, fp64"),
+    "c5": (3, 160, 6, False, "cart", False, "fp64", 4,
+           "C5: 3D SIPG, Cartesian 160^3, p=6, affine (compressed), fp64"),
+    "c5f32": (3, 160, 6, False, "cart", False, "fp32", 4,
+              "C5: 3D SIPG, Cartesian 160^3, p=6, affine (compressed), fp32"),
+    "c1": (3, 16, 3, True, "cart", False, "fp64", 0,
+           "C1: 3D SIPG, periodic Cartesian 16^3, p=3, fp64"),
+    "c2": (2, 256, 5, False, "cart", False, "fp64", 1,
+           "C2: 2D SIPG, Dirichlet Cartesian 256^2, p=5, fp64"),
+}
+# reference instrumented flop count per DoF (counters x W / applies,
+# bench.cpp:339), SURVEY.md s.8d
+REF_FLOPS_PER_DOF = {"c4": 240.0, "c3": 215.52, "c5": 260.82, "c5f32": 260.82,
+                     "c1": 198.0, "c2": 105.80}
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            pk = json.load(f)
+        return float(pk["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks and throttle reasons sampled during the timed region."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                mx = max(mx, float(parts[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+class RefBench:
+    """Reference CPU apply (oracle/_ref/libdgref.so = the unmodified
+    reference RankOperator + GhostExchanger over run_ranks threads,
+    bench.cpp:128-166) on a bounded sample of the workload: the same
+    configuration at a reduced cell count, all host cores as threaded
+    ranks, the better lane width of W in {4, 8}."""
+
+    def __init__(self, cfg_name, sample_cells=None):
+        from oracle import oracle as O
+        from oracle import reflib as R
+        d, n, p, periodic, kind, coef, prec, seed, label = CONFIGS[cfg_name]
+        cores = os.cpu_count() or 1
+        if sample_cells is None:
+            sample_cells = {3: 16, 2: 128}[d]
+        cells = [sample_cells] * d
+        self.n_ranks = min(cores, int(np.prod(cells)))
+        geo = None
+        if kind == "vertex":
+            P = O.Problem(d, cells, p, periodic=periodic, deform=("vertex", 0.1),
+                          coefficient=coef, n_ranks=1)
+            geo = {k: P.geom[k] for k in ("inv_jac_t", "jxw", "face_jxw", "face_jni",
+                                          "face_jne", "penalty")}
+            geo["compressed"] = False
+        best = None
+        for W in (4, 8):
+            w = R.World(d, cells, p, n_ranks=self.n_ranks, periodic=periodic, W=W, geometry=geo)
+            w.time(1)
+            t = min(w.time(1) for _ in range(3))
+            if best is None or t < best[0]:
+                best = (t, W, w)
+        t1, self.W, self.world = best
+        self.n_dofs = self.world.n_dofs
+        # applies per timed step: >= 0.5 s of CPU work (run_benchmark times
+        # ceil(0.02 s / est) applies per repetition, bench.cpp:309-319)
+        self.inner = max(1, int(np.ceil(0.5 / max(t1, 1e-6))))
+        self.sample = (f"{label.split(':')[0]} shape at {sample_cells}^{d} cells "
+                       f"({self.n_dofs} DoFs), reference RankOperator::apply, GL basis, "
+                       f"W={self.W}, R={self.n_ranks} threaded ranks (run_ranks + "
+                       f"GhostExchanger), {self.inner} applies per step")
+
+    def step(self):
+        """DoF/s of one timed step (self.inner applies)."""
+        return self.n_dofs * self.inner / self.world.time(self.inner)
+
+    def rate(self, reps=11):
+        """~10 s of CPU work: median of reps steps."""
+        return statistics.median(self.step() for _ in range(reps))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="dgx", choices=["dgx", "reference"])
+    ap.add_argument("--config", default="c4", choices=sorted(CONFIGS))
+    ap.add_argument("--cells", type=int, default=None, help="override cells per direction")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    ws, rank, local = dist_env()
+    d, n, p, periodic, kind, coef, prec, seed, label = CONFIGS[args.config]
+    if args.cells:
+        n = args.cells
+    n_dofs = n ** d * (p + 1) ** d
+    metric = "DG Laplacian apply throughput (DoFs/s)"
+    config = {"workload": label, "cells": [n] * d, "degree": p, "n_dofs": n_dofs,
+              "seed": seed, "partition": f"contiguous lexicographic slabs x{args.gpus}",
+              "l2": "inputs larger than L2 (no flush)"}
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        rb = RefBench(args.config)
+        for _ in range(args.warmup):
+            rb.step()
+        val = statistics.median(rb.step() for _ in range(args.steps))
+        info = {"cores": rb.n_ranks, "sample": rb.sample}
+        out = {"metric": metric, "value": val, "unit": "DoF/s", "impl": "reference",
+               "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+               "ms_per_step": n_dofs / val * 1e3, "higher_is_better": True,
+               "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+               "config": config,
+               "cpu_baseline": {"value": val, "unit": "DoF/s", "cores": info["cores"],
+                                "kind": "reference", "sample": info["sample"]},
+               "e2e": {"value": val, "unit": "DoF/s", "h2d_bytes_per_step": 0,
+                       "d2h_bytes_per_step": 0}}
+        print(json.dumps(out), flush=True)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_1711_03590_b200 as dgx
+
+    torch.cuda.set_device(local)
+    if ws > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    t_setup = time.time()
+    mesh = dgx.make_box_mesh(d, n, 0.0, periodic, 1)
+    faces = dgx.enumerate_faces(mesh)
+    part = dgx.partition_cells(mesh, ws)
+    dgx.assign_face_owners(mesh, faces, part)
+    geo = (dgx.Geometry(source="vertex_bump", vertex_bump_eps=0.1, coefficient="a1" if coef else None)
+           if kind == "vertex" else dgx.Geometry(source="mesh"))
+    op = dgx.RankOperator(mesh, part, faces, geo, dgx.OperatorConfig(d=d, p=p, precision=prec),
+                          rank, device=local)
+    lay = op.layout()
+    hooks = None
+    if ws > 1:
+        uid = [dgx.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        hooks = dgx.NcclExchanger(op, uid[0])
+    del faces
+    st = op.stats()
+    dt = torch.float32 if prec == "fp32" else torch.float64
+    esize = 4 if prec == "fp32" else 8
+    nq = lay.dofs_per_cell
+    # input: U[-1,1] from seed (std::mt19937 convention), this rank's slab
+    # plus its ghost cells (gathered from the same global stream)
+    b, e = lay.owned_cell_begin, lay.owned_cell_begin + lay.n_owned_cells
+    x_owned = dgx.random_vector(e * nq, seed)[b * nq:]
+    u_host = torch.empty(lay.total_size, dtype=dt).pin_memory()
+    u_host[: lay.owned_size] = torch.from_numpy(x_owned).to(dt)
+    del x_owned
+    u = u_host.to(f"cuda:{local}")
+    y = torch.empty_like(u)
+    y_host = torch.empty(lay.total_size, dtype=dt).pin_memory()
+    stream = torch.cuda.current_stream()
+    t_setup = time.time() - t_setup
+
+    def step():
+        op.apply(u, y, hooks=hooks, stream=stream)
+
+    def barrier():
+        if ws > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        step()
+    barrier()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        barrier()
+        ev0.record(stream)
+        for _ in range(args.steps):
+            step()
+        ev1.record(stream)
+        barrier()
+    t_ms = ev0.elapsed_time(ev1)
+    # per-step (= per-launch at N=1) durations for the roofline
+    times = []
+    for _ in range(min(args.steps, 5)):
+        a, bb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        step()
+        bb.record(stream)
+        bb.synchronize()
+        times.append(a.elapsed_time(bb))
+    t_max = torch.tensor([t_ms], dtype=torch.float64, device=f"cuda:{local}")
+    if ws > 1:
+        dist.all_reduce(t_max, op=dist.ReduceOp.MAX)
+    t_ms = float(t_max.item())
+    ms_per_step = t_ms / args.steps
+    value = n_dofs / (ms_per_step * 1e-3)
+
+    # end to end through the public API with host buffers: H2D of u, apply,
+    # D2H of y every step
+    e2e = None
+    if not args.no_e2e:
+        h2d = lay.total_size * esize if ws == 1 else lay.owned_size * esize
+        d2h = lay.owned_size * esize
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.steps):
+            u[: h2d // esize].copy_(u_host[: h2d // esize], non_blocking=True)
+            step()
+            y_host[: d2h // esize].copy_(y[: d2h // esize], non_blocking=True)
+        e1.record(stream)
+        barrier()
+        te = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=f"cuda:{local}")
+        if ws > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        e2e = {"value": n_dofs / (float(te.item()) / args.steps * 1e-3), "unit": "DoF/s",
+               "h2d_bytes_per_step": int(h2d) * ws, "d2h_bytes_per_step": int(d2h) * ws}
+
+    hbm, hbm_kind = peaks()
+    alg_bytes = st["bytes_vectors"] + st["bytes_cell_geometry"] + st["bytes_face_geometry"]
+    launch_ms = statistics.median(times)
+    achieved = alg_bytes / (launch_ms * 1e-3) / 1e9
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", f"traffic_{args.config}.json")
+    if os.path.exists(prof):
+        try:
+            traffic = json.load(open(prof)).get("traffic_bytes_per_launch")
+        except Exception:
+            traffic = None
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                "frac": achieved / hbm, "traffic": traffic,
+                "peak_source": hbm_kind, "algorithmic_bytes_per_launch": alg_bytes,
+                "bytes_per_dof": alg_bytes / (lay.owned_size),
+                "launch_ms": launch_ms,
+                "fp64_flops_per_dof_ref_counters": REF_FLOPS_PER_DOF.get(args.config)}
+
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        try:
+            rb = RefBench(args.config)
+            cpu = {"value": rb.rate(), "unit": "DoF/s", "cores": rb.n_ranks,
+                   "kind": "reference", "sample": rb.sample + ", median of 11 steps"}
+        except Exception as ex:  # reported, never silently replaced
+            cpu = {"value": None, "unit": "DoF/s", "cores": 0, "kind": "reference",
+                   "sample": f"unavailable: {ex}"}
+
+    if rank == 0:
+        out = {"metric": metric, "value": value, "unit": "DoF/s", "n_gpus": ws,
+               "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
+               "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+               "dtype": "f32" if prec == "fp32" else "f64", "data": "synthetic",
+               "config": config, "e2e": e2e,
+               "gpu_launches": int(args.steps * st["kernel_launches_per_apply"] +
+                                   (args.steps * (1 + len(op.plans("send"))) if ws > 1 else 0)),
+               "roofline": roofline, "cpu_baseline": cpu, "clocks": clk.summary(),
+               "setup_s": t_setup}
+        print(json.dumps(out), flush=True)
+    if ws > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,130 @@
+// Device-side helpers shared by the operator implementation.
+#pragma once
+
+#include "setup.hpp"
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+namespace dgx
+{
+
+inline void cuda_check(cudaError_t e, const char *what)
+{
+  if (e != cudaSuccess)
+    fail(Code::cuda_error, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+// Owning device allocation (no torch types cross the C ABI; the operator
+// owns geometry and task tables, the caller owns the vectors).
+template <typename T>
+class DeviceArray
+{
+public:
+  DeviceArray() = default;
+  explicit DeviceArray(size_t n) { resize(n); }
+  DeviceArray(const DeviceArray &) = delete;
+  DeviceArray &operator=(const DeviceArray &) = delete;
+  DeviceArray(DeviceArray &&o) noexcept : p_(o.p_), n_(o.n_) { o.p_ = nullptr; o.n_ = 0; }
+  DeviceArray &operator=(DeviceArray &&o) noexcept
+  {
+    if (this != &o)
+      {
+        release();
+        p_ = o.p_;
+        n_ = o.n_;
+        o.p_ = nullptr;
+        o.n_ = 0;
+      }
+    return *this;
+  }
+  ~DeviceArray() { release(); }
+
+  void resize(size_t n)
+  {
+    release();
+    if (n)
+      cuda_check(cudaMalloc(&p_, n * sizeof(T)), "cudaMalloc");
+    n_ = n;
+  }
+  void upload(const T *h, size_t n, cudaStream_t s = nullptr)
+  {
+    if (n != n_)
+      resize(n);
+    if (n)
+      cuda_check(cudaMemcpyAsync(p_, h, n * sizeof(T), cudaMemcpyHostToDevice, s),
+                 "upload");
+  }
+  void upload(const std::vector<T> &v, cudaStream_t s = nullptr) { upload(v.data(), v.size(), s); }
+  std::vector<T> download() const
+  {
+    std::vector<T> h(n_);
+    if (n_)
+      cuda_check(cudaMemcpy(h.data(), p_, n_ * sizeof(T), cudaMemcpyDeviceToHost), "download");
+    return h;
+  }
+  T *get() const { return p_; }
+  size_t size() const { return n_; }
+  size_t bytes() const { return n_ * sizeof(T); }
+
+private:
+  void release()
+  {
+    if (p_)
+      cudaFree(p_);
+    p_ = nullptr;
+    n_ = 0;
+  }
+  T *p_ = nullptr;
+  size_t n_ = 0;
+};
+
+namespace dev
+{
+template <typename Real>
+struct ApplyParams;
+}
+
+// sipg.cu
+void upload_tables(int K);
+int kernel_cells_per_cta(int D, int K);
+template <typename Real>
+void launch_apply(int D, int K, bool compressed, const dev::ApplyParams<Real> &prm,
+                  cudaStream_t s);
+
+// geometry.cu -- device precompute of the g3 arrays from mapping support
+// points (reference geometry.cpp:36-150,248-522), written straight into the
+// device SoA layout the apply kernel reads.
+struct GeometryJob
+{
+  int d = 3, k = 2, m = 1;
+  bool compress = false;
+  int coefficient = 0;  // 1: a(x) = 1 + 0.5 sin(pi x) cos(pi y) folded in
+  double cart_volume = 0; // > 0: Cartesian mesh, every cell has this volume
+  const double *support = nullptr; // device [n_slots][(m+1)^d][d]
+  int n_slots = 0;       // local cells with support points
+  int n_geo_cells = 0;   // owned cells, slots 0..n_geo_cells-1
+  long long n_faces = 0; // faces computed on this rank
+  const int4 *faces = nullptr; // device: (slot-, slot+ or -1, fn-, fn+)
+  double *cell_geo = nullptr;  // [n_geo][d*d+1][k^d] or [n_geo][d*d+1]
+  double *face_geo = nullptr;  // [n_faces][2d+1][k^{d-1}]
+  double *penalty = nullptr;   // [n_faces]
+  double *volume = nullptr;    // scratch [n_slots]
+};
+void run_geometry(const GeometryJob &job, cudaStream_t s);
+
+// exchange.cu -- halo pack / compress kernels (whole cells: GL basis with
+// first derivatives ships all k^d dofs, ghost_exchange.cpp:49-96).
+template <typename T>
+void launch_gather_cells(const T *src, const int *slots, int n_cells, long long nq, T *dst,
+                         cudaStream_t s);
+template <typename T>
+void launch_scatter_add_cells(T *dst, const int *slots, int n_cells, long long nq, const T *src,
+                              cudaStream_t s);
+template <typename Real>
+void launch_convert(const double *src, Real *dst, long long n, cudaStream_t s);
+
+} // namespace dgx

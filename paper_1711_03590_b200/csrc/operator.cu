@@ -1,0 +1,493 @@
+// Rank operator: setup (layout, cell tasks, device geometry) and apply.
+// Mirrors RankOperator / OperatorImpl (reference operators.cpp:89-264).
+#include "operator.hpp"
+#include "sipg_kernel.cuh"
+
+#include <algorithm>
+#include <cstring>
+
+namespace dgx
+{
+
+namespace
+{
+MeshDesc to_mesh(const dgx_mesh &m)
+{
+  MeshDesc md;
+  md.d = m.d;
+  for (int a = 0; a < 3; ++a)
+    {
+      md.cells[a] = a < m.d ? m.cells_per_dim[a] : 1;
+      md.lo[a] = m.lo[a];
+      md.hi[a] = m.hi[a];
+      md.periodic[a] = m.periodic[a] != 0;
+    }
+  md.amplitude = m.deform_amplitude;
+  md.mapping_degree = std::max(1, m.mapping_degree);
+  for (int s = 0; s < 6; ++s)
+    md.dirichlet_id[s] = m.dirichlet_id[s];
+  md.check();
+  return md;
+}
+} // namespace
+
+Operator::Operator(const dgx_setup &s, int device) : device_(device)
+{
+  const dgx_config &c = s.config;
+  if (c.basis != 0)
+    fail(Code::invalid_argument,
+         "RankOperator: only the nodal Gauss-Lobatto basis is implemented on the device");
+  if (c.geometry_variant != 3)
+    fail(Code::invalid_argument, "RankOperator: only geometry variant g3 is implemented");
+  if (c.d != s.mesh.d)
+    fail(Code::invalid_argument, "RankOperator: mesh dimension mismatch");
+  if (c.W != 1 && c.W != 2 && c.W != 4 && c.W != 8)
+    fail(Code::invalid_argument, "RankOperator: unsupported lane count");
+  if (c.precision != 0 && c.precision != 1)
+    fail(Code::invalid_argument, "RankOperator: precision must be 0 (fp64) or 1 (fp32)");
+  mesh_ = to_mesh(s.mesh);
+  d_ = c.d;
+  p_ = c.p;
+  k_ = c.p + 1;
+  if (c.p < 1 || c.p > 10)
+    fail(Code::invalid_argument, "RankOperator: supported degrees are 1..10");
+  precision_ = c.precision;
+  nq_ = 1;
+  for (int a = 0; a < d_; ++a)
+    nq_ *= k_;
+  nqf_ = nq_ / k_;
+
+  host_only_ = device_ < 0;
+  if (!host_only_)
+    cuda_check(cudaSetDevice(device_), "cudaSetDevice");
+
+  if (!s.faces || s.n_faces <= 0)
+    fail(Code::invalid_argument, "RankOperator: empty face list");
+  std::vector<RawFace> faces(s.n_faces);
+  std::memcpy(faces.data(), s.faces, sizeof(RawFace) * s.n_faces);
+  const long long nc = mesh_.n_cells();
+  for (const RawFace &f : faces)
+    if (f.interior_cell >= nc || (!f.at_boundary() && f.exterior_cell >= nc) ||
+        f.interior_face_number >= 2 * d_ ||
+        (!f.at_boundary() && f.exterior_face_number >= 2 * d_))
+      fail(Code::invalid_argument, "RankOperator: face references an invalid cell or face");
+
+  Partition part;
+  if (s.n_ranks < 1)
+    fail(Code::invalid_argument, "RankOperator: n_ranks must be >= 1");
+  if (s.cell_owner && s.rank_cell_range && s.face_owner)
+    {
+      part.n_ranks = s.n_ranks;
+      part.cell_owner.assign(s.cell_owner, s.cell_owner + nc);
+      for (int r = 0; r < s.n_ranks; ++r)
+        part.ranges.emplace_back(s.rank_cell_range[2 * r], s.rank_cell_range[2 * r + 1]);
+      part.face_owner.assign(s.face_owner, s.face_owner + s.n_faces);
+    }
+  else
+    part = make_partition(mesh_, faces, s.n_ranks);
+  n_ranks_ = part.n_ranks;
+  layout_ = build_layout(mesh_, faces, part, s.rank, k_);
+
+  build_tasks(faces, part);
+  if (host_only_)
+    return;
+  build_geometry(s, faces);
+  upload_tables(k_);
+}
+
+// Task lists. Owned cells whose computed faces never read a ghost form the
+// inner phase (overlappable with the ghost update, operators.cpp:314-317);
+// owned cells with a ghost-reading face and one "ghost-side" task per ghost
+// cell (the remote side of the faces this rank computes, later compressed
+// to the owner) form the coupled phase.
+void Operator::build_tasks(const std::vector<RawFace> &faces, const Partition &part)
+{
+  const int nfpc = 2 * d_;
+  const long long n_owned = layout_.n_owned;
+  const long long n_slots = n_owned + (long long)layout_.ghosts.size();
+  std::vector<long long> face_of(n_slots * nfpc, -1);
+  for (std::size_t f = 0; f < faces.size(); ++f)
+    {
+      const RawFace &rf = faces[f];
+      const long long s0 = layout_.slot(rf.interior_cell);
+      if (s0 >= 0)
+        face_of[s0 * nfpc + rf.interior_face_number] = (long long)f;
+      if (!rf.at_boundary())
+        {
+          const long long s1 = layout_.slot(rf.exterior_cell);
+          if (s1 >= 0)
+            face_of[s1 * nfpc + rf.exterior_face_number] = (long long)f;
+        }
+    }
+  std::vector<int> face_local(faces.size(), -1);
+  for (std::size_t i = 0; i < layout_.my_faces.size(); ++i)
+    face_local[layout_.my_faces[i]] = static_cast<int>(i);
+
+  std::vector<int> slot_inner, slot_coupled, geo_inner, geo_coupled;
+  std::vector<int2> tf_inner, tf_coupled;
+  auto make_task = [&](long long slot, bool owned, std::vector<int2> &tf) {
+    bool coupled = false;
+    const std::uint32_t gcell =
+      owned ? layout_.owned_begin + (std::uint32_t)slot : layout_.ghosts[slot - n_owned];
+    for (int phi = 0; phi < nfpc; ++phi)
+      {
+        const long long f = face_of[slot * nfpc + phi];
+        int2 e = make_int2(-2, 0);
+        if (f < 0)
+          {
+            if (owned)
+              fail(Code::logic_error, "layout: owned cell without a face on every side");
+          }
+        else if (part.face_owner[f] == layout_.rank)
+          {
+            const RawFace &rf = faces[f];
+            const int side =
+              (rf.interior_cell == gcell && rf.interior_face_number == phi) ? 0 : 1;
+            if (rf.at_boundary())
+              e.x = -1;
+            else
+              {
+                const std::uint32_t other = side == 0 ? rf.exterior_cell : rf.interior_cell;
+                const long long os = layout_.slot(other);
+                if (os < 0)
+                  fail(Code::logic_error, "layout: face neighbour absent on this rank");
+                e.x = static_cast<int>(os);
+                if (os >= n_owned)
+                  coupled = true;
+              }
+            e.y = face_local[f] | (side << 30);
+          }
+        tf.push_back(e);
+      }
+    return coupled;
+  };
+
+  for (long long s = 0; s < n_owned; ++s)
+    {
+      std::vector<int2> tf;
+      const bool coupled = make_task(s, true, tf);
+      auto &sl = coupled ? slot_coupled : slot_inner;
+      auto &gl = coupled ? geo_coupled : geo_inner;
+      auto &fl = coupled ? tf_coupled : tf_inner;
+      sl.push_back(static_cast<int>(s));
+      gl.push_back(static_cast<int>(s));
+      fl.insert(fl.end(), tf.begin(), tf.end());
+    }
+  for (long long s = n_owned; s < n_slots; ++s)
+    {
+      std::vector<int2> tf;
+      make_task(s, false, tf);
+      slot_coupled.push_back(static_cast<int>(s));
+      geo_coupled.push_back(-1);
+      tf_coupled.insert(tf_coupled.end(), tf.begin(), tf.end());
+    }
+  n_inner_ = static_cast<int>(slot_inner.size());
+  n_coupled_ = static_cast<int>(slot_coupled.size());
+  slot_inner.insert(slot_inner.end(), slot_coupled.begin(), slot_coupled.end());
+  geo_inner.insert(geo_inner.end(), geo_coupled.begin(), geo_coupled.end());
+  tf_inner.insert(tf_inner.end(), tf_coupled.begin(), tf_coupled.end());
+  if (!host_only_)
+    {
+      task_slot_.upload(slot_inner);
+      task_geo_.upload(geo_inner);
+      task_face_.upload(tf_inner);
+    }
+  host_task_slot_ = slot_inner;
+  host_task_geo_ = geo_inner;
+  host_task_face_ = tf_inner;
+
+  // exchange plans: owned slots of the cells every neighbour receives
+  std::vector<int> ss;
+  send_offsets_.assign(1, 0);
+  for (const NeighborPlan &np : layout_.send)
+    {
+      for (std::uint32_t c : np.cells)
+        ss.push_back(static_cast<int>(layout_.slot(c)));
+      send_offsets_.push_back((long long)ss.size());
+    }
+  if (!host_only_)
+    send_slots_.upload(ss);
+  recv_offsets_.assign(1, 0);
+  long long pos = 0;
+  for (const NeighborPlan &np : layout_.recv)
+    {
+      for (std::uint32_t c : np.cells)
+        {
+          if (layout_.slot(c) != n_owned + pos)
+            recv_contiguous_ = false;
+          ++pos;
+        }
+      recv_offsets_.push_back(pos);
+    }
+  if (pos != (long long)layout_.ghosts.size())
+    recv_contiguous_ = false;
+}
+
+void Operator::build_geometry(const dgx_setup &s, const std::vector<RawFace> &faces)
+{
+  const dgx_geometry &g = s.geometry;
+  const long long n_owned = layout_.n_owned;
+  const long long n_slots = n_owned + (long long)layout_.ghosts.size();
+  const long long nmy = (long long)layout_.my_faces.size();
+  const int ncomp = d_ * d_ + 1;
+  std::vector<std::uint32_t> slot_cells(n_slots);
+  for (long long i = 0; i < n_owned; ++i)
+    slot_cells[i] = layout_.owned_begin + (std::uint32_t)i;
+  for (std::size_t i = 0; i < layout_.ghosts.size(); ++i)
+    slot_cells[n_owned + i] = layout_.ghosts[i];
+
+  if (g.source == DGX_GEOMETRY_HOST_ARRAYS)
+    {
+      if (g.coefficient)
+        fail(Code::invalid_argument, "geometry: fold the coefficient into the host arrays");
+      if (!g.inv_jac_t || !g.jxw || !g.face_jxw || !g.face_jni || !g.face_jne || !g.penalty)
+        fail(Code::invalid_argument, "geometry: missing host arrays");
+      compressed_ = g.compressed != 0;
+      const long long nrec = compressed_ ? 1 : nq_;
+      std::vector<double> cg((size_t)n_owned * ncomp * nrec);
+      for (long long c = 0; c < n_owned; ++c)
+        {
+          const long long gc = layout_.owned_begin + c;
+          for (long long r = 0; r < nrec; ++r)
+            {
+              const double *jit = g.inv_jac_t + (gc * nrec + r) * d_ * d_;
+              for (int i = 0; i < d_ * d_; ++i)
+                cg[(c * ncomp + i) * nrec + r] = jit[i];
+              cg[(c * ncomp + d_ * d_) * nrec + r] = g.jxw[gc * nrec + r];
+            }
+        }
+      std::vector<double> fg((size_t)nmy * (2 * d_ + 1) * nqf_), pen(nmy);
+      for (long long i = 0; i < nmy; ++i)
+        {
+          const long long f = layout_.my_faces[i];
+          for (long long q = 0; q < nqf_; ++q)
+            {
+              double *o = fg.data() + i * (2 * d_ + 1) * nqf_ + q;
+              o[0] = g.face_jxw[f * nqf_ + q];
+              for (int b = 0; b < d_; ++b)
+                {
+                  o[(1 + b) * nqf_] = g.face_jni[(f * nqf_ + q) * d_ + b];
+                  o[(1 + d_ + b) * nqf_] = g.face_jne[(f * nqf_ + q) * d_ + b];
+                }
+            }
+          pen[i] = g.penalty[f];
+        }
+      cell_geo_.upload(cg);
+      face_geo_.upload(fg);
+      penalty_.upload(pen);
+    }
+  else
+    {
+      std::vector<double> support;
+      int m = 1;
+      bool cartesian = false;
+      switch (g.source)
+        {
+        case DGX_GEOMETRY_MESH:
+          m = mesh_.mapping_degree;
+          support = reference_support(mesh_, slot_cells);
+          cartesian = mesh_.amplitude == 0.0;
+          break;
+        case DGX_GEOMETRY_VERTEX_BUMP:
+          m = 1;
+          support = vertex_bump_support(mesh_, g.vertex_bump_eps, slot_cells);
+          cartesian = g.vertex_bump_eps == 0.0;
+          break;
+        case DGX_GEOMETRY_SUPPORT:
+          {
+            if (!g.support_points)
+              fail(Code::invalid_argument, "geometry: missing support points");
+            m = std::max(1, g.support_degree);
+            long long pp = 1;
+            for (int a = 0; a < d_; ++a)
+              pp *= m + 1;
+            support.resize((size_t)n_slots * pp * d_);
+            for (long long i = 0; i < n_slots; ++i)
+              std::memcpy(support.data() + i * pp * d_,
+                          g.support_points + (long long)slot_cells[i] * pp * d_,
+                          sizeof(double) * pp * d_);
+            cartesian = g.cartesian != 0;
+            break;
+          }
+        default:
+          fail(Code::invalid_argument, "geometry: unknown source");
+        }
+      if (g.coefficient != 0 && g.coefficient != 1)
+        fail(Code::invalid_argument, "geometry: unknown coefficient");
+      compressed_ = cartesian && !g.coefficient;
+      DeviceArray<double> dsup;
+      dsup.upload(support);
+      std::vector<int4> fl(nmy);
+      for (long long i = 0; i < nmy; ++i)
+        {
+          const RawFace &rf = faces[layout_.my_faces[i]];
+          fl[i] = make_int4(static_cast<int>(layout_.slot(rf.interior_cell)),
+                            rf.at_boundary() ? -1 : static_cast<int>(layout_.slot(rf.exterior_cell)),
+                            rf.interior_face_number, rf.exterior_face_number);
+        }
+      DeviceArray<int4> dfl;
+      dfl.upload(fl);
+      DeviceArray<double> vol(n_slots);
+      cell_geo_.resize((size_t)n_owned * ncomp * (compressed_ ? 1 : nq_));
+      face_geo_.resize((size_t)nmy * (2 * d_ + 1) * nqf_);
+      penalty_.resize(nmy);
+      GeometryJob job;
+      job.d = d_;
+      job.k = k_;
+      job.m = m;
+      job.compress = compressed_;
+      job.coefficient = g.coefficient;
+      if (cartesian)
+        {
+          double v = 1.0;
+          for (int a = 0; a < d_; ++a)
+            v *= (mesh_.hi[a] - mesh_.lo[a]) / mesh_.cells[a];
+          job.cart_volume = v;
+        }
+      job.support = dsup.get();
+      job.n_slots = static_cast<int>(n_slots);
+      job.n_geo_cells = static_cast<int>(n_owned);
+      job.n_faces = nmy;
+      job.faces = dfl.get();
+      job.cell_geo = cell_geo_.get();
+      job.face_geo = face_geo_.get();
+      job.penalty = penalty_.get();
+      job.volume = vol.get();
+      run_geometry(job, nullptr);
+    }
+  if (precision_ == 1)
+    {
+      cell_geo_f_.resize(cell_geo_.size());
+      face_geo_f_.resize(face_geo_.size());
+      penalty_f_.resize(penalty_.size());
+      launch_convert<float>(cell_geo_.get(), cell_geo_f_.get(), cell_geo_.size(), nullptr);
+      launch_convert<float>(face_geo_.get(), face_geo_f_.get(), face_geo_.size(), nullptr);
+      launch_convert<float>(penalty_.get(), penalty_f_.get(), penalty_.size(), nullptr);
+      cuda_check(cudaDeviceSynchronize(), "convert geometry");
+    }
+  cuda_check(cudaDeviceSynchronize(), "geometry setup");
+}
+
+template <typename Real>
+void Operator::launch_range(int begin, int count, const Real *u, Real *y, cudaStream_t s)
+{
+  if (count <= 0)
+    return;
+  dev::ApplyParams<Real> prm;
+  prm.u = u;
+  prm.y = y;
+  if constexpr (sizeof(Real) == 8)
+    {
+      prm.cell_geo = cell_geo_.get();
+      prm.face_geo = face_geo_.get();
+      prm.penalty = penalty_.get();
+    }
+  else
+    {
+      prm.cell_geo = cell_geo_f_.get();
+      prm.face_geo = face_geo_f_.get();
+      prm.penalty = penalty_f_.get();
+    }
+  prm.task_slot = task_slot_.get() + begin;
+  prm.task_geo = task_geo_.get() + begin;
+  prm.task_face = task_face_.get() + (long long)begin * 2 * d_;
+  prm.n_tasks = count;
+  launch_apply<Real>(d_, k_, compressed_, prm, s);
+}
+
+void Operator::apply_phase(int phase, const void *u, void *y, cudaStream_t s, bool fp32)
+{
+  if (fp32 != (precision_ == 1))
+    fail(Code::invalid_argument, "apply: precision does not match the operator config");
+  if (host_only_)
+    fail(Code::invalid_argument, "apply: operator was created host-only (device < 0)");
+  if (u == y)
+    fail(Code::invalid_argument, "apply: source and destination must differ");
+  cuda_check(cudaSetDevice(device_), "cudaSetDevice");
+  const int b = phase == 1 ? 0 : n_inner_;
+  const int n = phase == 1 ? n_inner_ : n_coupled_;
+  if (phase != 1 && phase != 2)
+    fail(Code::invalid_argument, "apply_phase: phase must be 1 or 2");
+  if (fp32)
+    {
+#ifdef DGX_WITH_FP32
+      launch_range<float>(b, n, static_cast<const float *>(u), static_cast<float *>(y), s);
+#else
+      fail(Code::invalid_argument, "apply: library built without fp32 kernels");
+#endif
+    }
+  else
+    launch_range<double>(b, n, static_cast<const double *>(u), static_cast<double *>(y), s);
+}
+
+// RankOperator::apply (operators.cpp:217-264) with the exchange hooks.
+void Operator::apply(void *u, void *y, const dgx_hooks *hooks, cudaStream_t s, bool fp32)
+{
+  const bool have_ghosts = !layout_.ghosts.empty();
+  auto call = [&](dgx_hook_fn fn, void *v, const char *what) {
+    const dgx_status st = fn(hooks->ctx, v, static_cast<void *>(s));
+    if (st != DGX_OK)
+      fail(static_cast<Code>(st), std::string(what) + " hook failed");
+  };
+  if (hooks && hooks->start_ghost_update)
+    call(hooks->start_ghost_update, u, "start_ghost_update");
+  else if (have_ghosts)
+    fail(Code::logic_error, "apply: layout has ghost cells but no exchange hooks were given");
+  apply_phase(1, u, y, s, fp32);
+  if (n_coupled_ > 0)
+    {
+      if (hooks && hooks->finish_ghost_update)
+        call(hooks->finish_ghost_update, u, "finish_ghost_update");
+      else if (have_ghosts)
+        fail(Code::logic_error,
+             "apply: ghost-coupled face reached without a way to finish the ghost update");
+      apply_phase(2, u, y, s, fp32);
+    }
+  if (hooks && hooks->compress)
+    call(hooks->compress, y, "compress");
+}
+
+void Operator::accumulate_plan(int idx, const double *contrib, double *y, cudaStream_t s)
+{
+  if (idx < 0 || idx >= (int)layout_.send.size())
+    fail(Code::invalid_argument, "accumulate_plan: plan index out of range");
+  const long long b = send_offsets_[idx], e = send_offsets_[idx + 1];
+  launch_scatter_add_cells(y, send_slots_.get() + b, static_cast<int>(e - b), nq_, contrib, s);
+}
+
+std::vector<double> Operator::geometry(int which) const
+{
+  if (host_only_ && which != 3)
+    fail(Code::invalid_argument, "geometry: operator was created host-only");
+  switch (which)
+    {
+    case 0: return cell_geo_.download();
+    case 1: return face_geo_.download();
+    case 2: return penalty_.download();
+    case 3:
+      {
+        std::vector<double> v(layout_.my_faces.begin(), layout_.my_faces.end());
+        return v;
+      }
+    default: fail(Code::invalid_argument, "geometry: unknown array");
+    }
+}
+
+dgx_stats Operator::stats() const
+{
+  dgx_stats st{};
+  st.n_tasks_inner = n_inner_;
+  st.n_tasks_coupled = n_coupled_;
+  st.n_faces = (long long)layout_.my_faces.size();
+  st.kernel_launches_per_apply = (n_inner_ > 0) + (n_coupled_ > 0);
+  const double es = precision_ == 1 ? 4.0 : 8.0;
+  st.bytes_vectors = 2.0 * es * (double)layout_.owned_size();
+  st.bytes_cell_geometry = es * (double)cell_geo_.size();
+  st.bytes_face_geometry = es * (double)(face_geo_.size() + penalty_.size());
+  st.cells_per_cta = kernel_cells_per_cta(d_, k_);
+  long long P = nq_ / k_;
+  st.threads_per_cta = static_cast<int>(st.cells_per_cta * P);
+  return st;
+}
+
+} // namespace dgx

@@ -1,0 +1,76 @@
+// The rank operator: host setup products plus the device state of one
+// B200 SIPG-Laplacian apply (the C ABI's dgx_op).
+#pragma once
+
+#include "device.hpp"
+#include "setup.hpp"
+
+#include "../../include/dgx.h"
+
+#include <memory>
+#include <vector>
+
+namespace dgx
+{
+
+class Operator
+{
+public:
+  Operator(const dgx_setup &s, int device);
+
+  void apply(void *u, void *y, const dgx_hooks *hooks, cudaStream_t stream, bool fp32);
+  // phase 1: inner tasks; phase 2: ghost-coupled + ghost-side tasks
+  void apply_phase(int phase, const void *u, void *y, cudaStream_t stream, bool fp32);
+  void accumulate_plan(int idx, const double *contrib, double *y, cudaStream_t s);
+
+  const RankLayout &layout() const { return layout_; }
+  int d() const { return d_; }
+  int k() const { return k_; }
+  int precision() const { return precision_; }
+  int device() const { return device_; }
+  int n_ranks() const { return n_ranks_; }
+  long long nq() const { return nq_; }
+  bool compressed() const { return compressed_; }
+  bool host_only() const { return host_only_; }
+  // task lists as built on the host: slot, geometry record, 2d face entries
+  const std::vector<int> &host_task_slot() const { return host_task_slot_; }
+  const std::vector<int> &host_task_geo() const { return host_task_geo_; }
+  const std::vector<int2> &host_task_face() const { return host_task_face_; }
+  int n_inner() const { return n_inner_; }
+
+  std::vector<double> geometry(int which) const;
+  dgx_stats stats() const;
+
+  // send-plan owned slots (device) with per-plan offsets, for the transports
+  const DeviceArray<int> &send_slots() const { return send_slots_; }
+  const std::vector<long long> &send_offsets() const { return send_offsets_; }
+  const std::vector<long long> &recv_offsets() const { return recv_offsets_; }
+  bool recv_contiguous() const { return recv_contiguous_; }
+
+private:
+  void build_tasks(const std::vector<RawFace> &faces, const Partition &part);
+  void build_geometry(const dgx_setup &s, const std::vector<RawFace> &faces);
+  template <typename Real>
+  void launch_range(int begin, int count, const Real *u, Real *y, cudaStream_t s);
+
+  MeshDesc mesh_;
+  int d_ = 3, p_ = 1, k_ = 2, precision_ = 0, device_ = 0, n_ranks_ = 1;
+  long long nq_ = 0, nqf_ = 0;
+  RankLayout layout_;
+  bool compressed_ = false;
+  bool host_only_ = false;
+  std::vector<int> host_task_slot_, host_task_geo_;
+  std::vector<int2> host_task_face_;
+
+  DeviceArray<double> cell_geo_, face_geo_, penalty_;
+  DeviceArray<float> cell_geo_f_, face_geo_f_, penalty_f_;
+  DeviceArray<int> task_slot_, task_geo_;
+  DeviceArray<int2> task_face_;
+  int n_inner_ = 0, n_coupled_ = 0;
+
+  DeviceArray<int> send_slots_;
+  std::vector<long long> send_offsets_, recv_offsets_; // in cells, size plans+1
+  bool recv_contiguous_ = true;
+};
+
+} // namespace dgx

@@ -1,0 +1,289 @@
+"""GPU parity: the CUDA path (through the C ABI) against the reference.
+
+* golden fixtures produced by the unmodified reference (single rank and
+  R ranks; per-rank results through the split phases + a serial compress,
+  the reference's SerialRanks pattern, tests/test_operators.cpp:446-535);
+* the C restatement oracle on random configurations, p = 1..10, 2D and 3D,
+  Cartesian / curved / BASELINE vertex deformation / folded a(x);
+* device geometry against the reference's precompute_geometry;
+* size-independent properties at BASELINE sizes (symmetry, linearity,
+  constants in the kernel on periodic meshes, bitwise determinism);
+* fp32 against fp64 at 1e-5.
+Tolerances: rel L_inf and rel L2 <= 1e-12 (fp64), 1e-5 (fp32), as north_star
+states.
+"""
+import ctypes as C
+
+import numpy as np
+import pytest
+
+from conftest import Case, cuda_available, golden_names, rel_l2, rel_linf
+
+pytestmark = pytest.mark.gpu
+
+NAMES = golden_names()
+TOL64 = 1e-12
+TOL32 = 1e-5
+
+
+@pytest.fixture(scope="module")
+def torch():
+    import torch as t
+    if not t.cuda.is_available():
+        pytest.skip("no CUDA device")
+    return t
+
+
+def dgx():
+    import paper_1711_03590_b200 as m
+    return m
+
+
+def geometry_of(c: Case):
+    G = dgx().Geometry
+    if c.vertex:
+        return G(source="vertex_bump", vertex_bump_eps=c.eps,
+                 coefficient="a1" if c.coefficient else None)
+    return G(source="mesh")
+
+
+def build(c: Case, rank=0, n_ranks=None, precision="fp64", p=None):
+    D = dgx()
+    mesh = D.make_box_mesh(c.d, c.cells, c.amplitude, c.periodic, c.m)
+    faces = D.enumerate_faces(mesh)
+    part = D.partition_cells(mesh, n_ranks or c.n_ranks)
+    D.assign_face_owners(mesh, faces, part)
+    cfg = D.OperatorConfig(d=c.d, p=p or c.p, precision=precision)
+    return D.RankOperator(mesh, part, faces, geometry_of(c), cfg, rank), part
+
+
+def apply_single(torch, op, x, dtype=None):
+    dtype = dtype or torch.float64
+    u = torch.tensor(x, dtype=dtype, device="cuda")
+    y = torch.empty_like(u)
+    op.apply(u, y)
+    torch.cuda.synchronize()
+    return y.double().cpu().numpy()
+
+
+def apply_serial_ranks(torch, ops, parts, x, nq, return_local=False):
+    """SerialRanks (reference tests/test_operators.cpp:446-535): ghost fill by
+    copy, both phases on the device per rank, compress on the host."""
+    y = np.zeros_like(x)
+    local = []
+    for r, op in enumerate(ops):
+        lay = op.layout()
+        b = lay.owned_cell_begin
+        e = b + lay.n_owned_cells
+        u_loc = np.concatenate([x[b * nq:e * nq]] +
+                               [x[g * nq:(g + 1) * nq] for g in lay.ghost_global_cells])
+        u = torch.tensor(u_loc, device="cuda")
+        yl = torch.full_like(u, float("nan"))
+        op.apply_phase(1, u, yl)
+        op.apply_phase(2, u, yl)
+        torch.cuda.synchronize()
+        y_loc = yl.cpu().numpy()
+        local.append((u_loc, y_loc))
+        y[b * nq:e * nq] += y_loc[: (e - b) * nq]
+        for i, g in enumerate(lay.ghost_global_cells):
+            y[g * nq:(g + 1) * nq] += y_loc[(e - b + i) * nq:(e - b + i + 1) * nq]
+    return (y, local) if return_local else y
+
+
+@pytest.mark.parametrize("name", NAMES)
+def test_golden_single_rank(torch, name):
+    c = Case(name)
+    op, _ = build(c, n_ranks=1)
+    for s in c.seeds:
+        y = apply_single(torch, op, c.g[f"x{s}"])
+        ref = c.g[f"y{s}"]
+        assert rel_linf(y, ref) < TOL64 and rel_l2(y, ref) < TOL64, (rel_linf(y, ref), rel_l2(y, ref))
+
+
+@pytest.mark.parametrize("name", [n for n in NAMES if n.endswith(("_r2", "_r3", "_r4", "_r7"))])
+def test_golden_rank_partitioned(torch, name):
+    from oracle import oracle as O
+    c = Case(name)
+    ops, parts = [], []
+    for r in range(c.n_ranks):
+        op, part = build(c, rank=r)
+        ops.append(op)
+        parts.append(part)
+    nq = (c.p + 1) ** c.d
+    x = c.g[f"x{c.seeds[0]}"]
+    y, local = apply_serial_ranks(torch, ops, parts, x, nq, return_local=True)
+    assert rel_linf(y, c.g[f"y{c.seeds[0]}"]) < TOL64
+    # per-rank state before compress (ghost slots hold remote contributions)
+    P = O.Problem(c.d, c.cells, c.p, periodic=c.periodic, deform=c.deform(),
+                  coefficient=c.coefficient, n_ranks=c.n_ranks)
+    for r, (u_loc, y_loc) in enumerate(local):
+        assert rel_linf(y_loc, P.apply_rank_local(r, u_loc)) < TOL64
+
+
+@pytest.mark.parametrize("name", [n for n in NAMES if n.startswith(("c1", "def3d", "c3", "c4", "c5", "def2d_p3"))])
+def test_device_geometry(torch, name):
+    c = Case(name)
+    if "geo_jxw" not in c.g:
+        pytest.skip("no geometry in fixture")
+    op, _ = build(c, n_ranks=1)
+    d, k = c.d, c.p + 1
+    nq, nqf = k ** d, k ** (d - 1)
+    cg = op.device_geometry(0)
+    nrec = 1 if bool(c.g.get("compressed", False)) else nq
+    nc = int(np.prod(c.cells))
+    cg = cg.reshape(nc, d * d + 1, nrec)
+    jit = c.g["geo_inv_jac_t"].reshape(nc, nrec, d * d).transpose(0, 2, 1)
+    jxw = c.g["geo_jxw"].reshape(nc, nrec)
+    tol = 1e-14 if c.coefficient else 0.0
+    assert rel_linf(cg[:, : d * d, :], jit) <= tol
+    assert rel_linf(cg[:, d * d, :], jxw) <= tol
+    fg = op.device_geometry(1).reshape(-1, 2 * d + 1, nqf)
+    fids = op.device_geometry(3).astype(np.int64)
+    assert rel_linf(fg[:, 0, :], c.g["geo_face_jxw"].reshape(-1, nqf)[fids]) <= tol
+    jni = c.g["geo_face_jni"].reshape(-1, nqf, d)[fids].transpose(0, 2, 1)
+    jne = c.g["geo_face_jne"].reshape(-1, nqf, d)[fids].transpose(0, 2, 1)
+    assert rel_linf(fg[:, 1:1 + d, :], jni) <= tol
+    assert rel_linf(fg[:, 1 + d:, :], jne) <= tol
+    assert rel_linf(op.device_geometry(2), c.g["geo_penalty"][fids]) <= max(tol, 1e-15)
+
+
+RANDOM = [
+    # d, cells, p, periodic, deform, coefficient, ranks
+    (2, [5, 4], p, bool(p % 2), ("reference", 0.05, 2), False, 1) for p in range(1, 11)
+] + [
+    (3, [3, 3, 2], p, bool(p % 2), ("reference", 0.04, 2), False, 1) for p in range(1, 11)
+] + [
+    (3, [4, 3, 3], 4, False, ("vertex", 0.1), False, 3),
+    (3, [3, 3, 4], 5, False, ("vertex", 0.1), True, 2),
+    (3, [4, 4, 3], 6, True, None, False, 4),
+    (2, [7, 5], 7, False, ("vertex", 0.1), True, 3),
+    (3, [2, 2, 2], 10, False, ("vertex", 0.1), False, 1),
+    (3, [1, 1, 3], 3, True, None, False, 1),
+]
+
+
+@pytest.mark.parametrize("cfg", RANDOM, ids=lambda c: f"d{c[0]}p{c[2]}r{c[6]}{'P' if c[3] else 'D'}{c[4][0][0] if c[4] else 'C'}{'a' if c[5] else ''}")
+def test_random_configs_against_oracle(torch, cfg):
+    from oracle import oracle as O
+    D = dgx()
+    d, cells, p, periodic, deform, coef, nr = cfg
+    P = O.Problem(d, cells, p, periodic=periodic, deform=deform, coefficient=coef, n_ranks=nr)
+    amp = deform[1] if deform and deform[0] == "reference" else 0.0
+    m = deform[2] if deform and deform[0] == "reference" else 1
+    mesh = D.make_box_mesh(d, cells, amp, periodic, m)
+    faces = D.enumerate_faces(mesh)
+    geo = (D.Geometry(source="vertex_bump", vertex_bump_eps=deform[1], coefficient="a1" if coef else None)
+           if deform and deform[0] == "vertex" else D.Geometry(source="mesh"))
+    x = O.random_vector(P.n_dofs, 1000 + p)
+    y_ref = P.apply(x)
+    ops = []
+    for r in range(nr):
+        part = D.partition_cells(mesh, nr)
+        D.assign_face_owners(mesh, faces, part)
+        ops.append(D.RankOperator(mesh, part, faces, geo, D.OperatorConfig(d=d, p=p), r))
+    if nr == 1:
+        y = apply_single(torch, ops[0], x)
+    else:
+        y = apply_serial_ranks(torch, ops, None, x, (p + 1) ** d)
+    assert rel_linf(y, y_ref) < TOL64 and rel_l2(y, y_ref) < TOL64, (rel_linf(y, y_ref), rel_l2(y, y_ref))
+
+
+class SerialHooks:
+    """dgx_hooks backed by ctypes callbacks; records the call order."""
+
+    def __init__(self):
+        from paper_1711_03590_b200 import _lib
+        self.calls = []
+
+        def mk(name):
+            def fn(ctx, vec, stream):
+                self.calls.append(name)
+                return 0
+            return _lib.HOOK_FN(fn)
+        self._fns = [mk("start"), mk("finish"), mk("compress")]
+        self._c = _lib.CHooks(None, *self._fns)
+
+    def c_hooks(self):
+        return self._c
+
+
+def test_hooks_protocol(torch):
+    c = Case("def3d_p3_m2_r2")
+    op, _ = build(c, rank=0)
+    n = op.layout().total_size
+    u = torch.zeros(n, dtype=torch.float64, device="cuda")
+    y = torch.zeros_like(u)
+    D = dgx()
+    with pytest.raises(D.DgxLogicError):
+        op.apply(u, y)  # ghosted layout without hooks (operators.cpp:238-240)
+    h = SerialHooks()
+    op.apply(u, y, hooks=h)
+    torch.cuda.synchronize()
+    assert h.calls == ["start", "finish", "compress"]
+    with pytest.raises(D.DgxInvalidArgument):
+        op.apply(u, u, hooks=h)
+
+
+def test_apply_host_pointers(torch):
+    c = Case("c5_cart_p6")
+    op, _ = build(c, n_ranks=1)
+    y = op.apply_host(c.g["x4"])
+    assert rel_linf(y, c.g["y4"]) < TOL64
+
+
+@pytest.mark.parametrize("name", ["c5_cart_p6", "c3_vertex_p4", "c1_periodic_cart_p3", "c2_dirichlet_cart_p10"])
+def test_fp32_against_fp64_reference(torch, name):
+    c = Case(name)
+    op, _ = build(c, n_ranks=1, precision="fp32")
+    s = c.seeds[0]
+    y = apply_single(torch, op, c.g[f"x{s}"], dtype=torch.float32)
+    assert rel_l2(y, c.g[f"y{s}"]) < TOL32
+
+
+def big_problem(torch, d, n, p, periodic, geometry):
+    D = dgx()
+    mesh = D.make_box_mesh(d, n, 0.0, periodic, 1)
+    faces = D.enumerate_faces(mesh)
+    part = D.partition_cells(mesh, 1)
+    D.assign_face_owners(mesh, faces, part)
+    return D.RankOperator(mesh, part, faces, geometry, D.OperatorConfig(d=d, p=p))
+
+
+def dot(a, b):
+    return float((a * b).sum().item())
+
+
+@pytest.mark.parametrize("shape", [
+    ("C1", 3, 16, 3, True, "cart"),
+    ("C3", 3, 64, 4, False, "vertex"),
+    ("C2", 2, 256, 7, False, "cart"),
+])
+def test_full_size_properties(torch, shape):
+    """Properties that hold at any size: symmetry v.Au = u.Av, linearity,
+    bitwise repeatability, and A 1 = 0 on periodic meshes (constants are in
+    the kernel of the SIP Laplacian; GL nodal coefficients of 1 are 1)."""
+    name, d, n, p, periodic, kind = shape
+    D = dgx()
+    geo = D.Geometry(source="vertex_bump", vertex_bump_eps=0.1) if kind == "vertex" else D.Geometry()
+    op = big_problem(torch, d, n, p, periodic, geo)
+    N = op.layout().total_size
+    g = torch.Generator(device="cuda").manual_seed(5)
+    u = torch.rand(N, dtype=torch.float64, device="cuda", generator=g) * 2 - 1
+    v = torch.rand(N, dtype=torch.float64, device="cuda", generator=g) * 2 - 1
+    Au, Av = torch.empty_like(u), torch.empty_like(u)
+    op.apply(u, Au)
+    op.apply(v, Av)
+    scale = float(torch.linalg.norm(u) * torch.linalg.norm(Av))
+    assert abs(dot(v, Au) - dot(u, Av)) < 1e-12 * scale
+    assert dot(u, Au) > 0  # positive (semi-)definite
+    w, Aw = 0.3 * u - 1.7 * v, torch.empty_like(u)
+    op.apply(w, Aw)
+    assert float(torch.linalg.norm(Aw - (0.3 * Au - 1.7 * Av))) < 1e-12 * float(torch.linalg.norm(Aw))
+    Au2 = torch.empty_like(u)
+    op.apply(u, Au2)
+    assert torch.equal(Au, Au2)
+    if periodic:
+        one = torch.ones_like(u)
+        A1 = torch.empty_like(u)
+        op.apply(one, A1)
+        assert float(A1.abs().max()) < 1e-11 * float(Au.abs().max())
