@@ -74,6 +74,17 @@ std::vector<double> build_table(int K)
   o += 2 * K;
   for (int j = 0; j < K; ++j)
     o[j] = t.qw[j];
+  o += K;
+  // rows (rf_s Dco)[j] = sum_q rf_s[q] Dco[q][j]: own normal-derivative
+  // trace from collocation values, and (Dco^T rf_s^T) for its transpose
+  for (int s = 0; s < 2; ++s)
+    for (int j = 0; j < K; ++j)
+      {
+        double acc = 0.0;
+        for (int q = 0; q < K; ++q)
+          acc += t.rf[s][q] * t.Dco[q * K + j];
+        o[s * K + j] = acc;
+      }
   return tab;
 }
 
@@ -84,7 +95,7 @@ template <typename Real, int D, int K, bool C>
 void launch_one(const dev::ApplyParams<Real> &prm, cudaStream_t s)
 {
   using KS = dev::KernelShape<D, K>;
-  const size_t smem = (size_t)KS::NC * KS::SM_CELL * sizeof(Real);
+  const size_t smem = (size_t)KS::SMEM_REALS * sizeof(Real);
   auto kern = dev::sipg_apply_kernel<Real, D, K, C>;
   static std::set<int> configured;
   int devid = 0;
@@ -96,6 +107,9 @@ void launch_one(const dev::ApplyParams<Real> &prm, cudaStream_t s)
         cuda_check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         (int)smem),
                    "cudaFuncSetAttribute");
+        cuda_check(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                        cudaSharedmemCarveoutMaxShared),
+                   "cudaFuncSetAttribute(carveout)");
         configured.insert(devid);
       }
   }
