@@ -9,7 +9,8 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libdgx.so")
+# DGX_LIB overrides the library path (kernel experiments only)
+LIB_PATH = os.environ.get("DGX_LIB") or os.path.join(_HERE, "libdgx.so")
 
 
 class DgxError(RuntimeError):

@@ -1,7 +1,7 @@
 // Rank operator: setup (layout, cell tasks, device geometry) and apply.
 // Mirrors RankOperator / OperatorImpl (reference operators.cpp:89-264).
 #include "operator.hpp"
-#include "sipg_kernel.cuh"
+#include "sipg_params.hpp"
 
 #include <algorithm>
 #include <cstring>
@@ -162,7 +162,37 @@ void Operator::build_tasks(const std::vector<RawFace> &faces, const Partition &p
     return coupled;
   };
 
-  for (long long s = 0; s < n_owned; ++s)
+  // Task order = traversal order of the owned cells. Lexicographic order
+  // puts the z-neighbour one cell layer (n_x n_y tasks) away, far beyond
+  // what L2 retains while the read-once geometry streams through it. Sweep
+  // z inside tiles of full x-rows and TILE_Y y-rows instead: the z-neighbour
+  // (and the shared face record) is then n_x TILE_Y tasks away and still in
+  // L2; only neighbours across the y tile edges are read twice from HBM.
+  std::vector<long long> order;
+  order.reserve(n_owned);
+  {
+    const int nx = mesh_.cells[0], ny = d_ == 3 ? mesh_.cells[1] : 1;
+    const long long layer = (long long)nx * ny;
+    const long long b = layout_.owned_begin, e = b + n_owned;
+    const int tile_y = d_ == 3 ? 8 : 1 << 30;
+    if (d_ == 3)
+      {
+        const long long z0 = b / layer, z1 = (e + layer - 1) / layer;
+        for (int ty = 0; ty < ny; ty += tile_y)
+          for (long long z = z0; z < z1; ++z)
+            for (int y = ty; y < std::min(ny, ty + tile_y); ++y)
+              for (int x = 0; x < nx; ++x)
+                {
+                  const long long c = z * layer + (long long)y * nx + x;
+                  if (c >= b && c < e)
+                    order.push_back(c - b);
+                }
+      }
+    else
+      for (long long s = 0; s < n_owned; ++s)
+        order.push_back(s);
+  }
+  for (long long s : order)
     {
       std::vector<int2> tf;
       const bool coupled = make_task(s, true, tf);

@@ -201,14 +201,17 @@ Tables1D make_tables(int p)
   t.qw = qg.weights;
   t.S.resize(k * k);
   t.Dco.resize(k * k);
+  t.D.resize(k * k);
   for (int q = 0; q < k; ++q)
     for (int j = 0; j < k; ++j)
       {
         t.S[q * k + j] = lagrange_value(nodes, j, qg.points[q]);
         t.Dco[q * k + j] = lagrange_derivative(qg.points, j, qg.points[q]);
+        t.D[q * k + j] = lagrange_derivative(nodes, j, qg.points[q]);
       }
   mirror_roundtrip(t.S, k, false);
   mirror_roundtrip(t.Dco, k, true);
+  mirror_roundtrip(t.D, k, true);
   for (int s = 0; s < 2; ++s)
     {
       const double x = s ? 1.0 : 0.0;

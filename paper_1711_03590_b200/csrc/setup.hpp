@@ -55,6 +55,7 @@ struct Tables1D
   int k = 0;
   std::vector<double> S;   // k x k, S[q][j] = phi_j(x_q)
   std::vector<double> Dco; // k x k, collocation derivative in the Gauss points
+  std::vector<double> D;   // k x k, D[q][j] = phi_j'(x_q) (nodal derivative)
   std::array<std::vector<double>, 2> Sf, Df; // nodal value / derivative rows at x=0,1
   // rf[s] = Sf[s] S^{-1}: extrapolation of Gauss-point values to the end
   // point s (exact for polynomials of degree < k).

@@ -9,12 +9,6 @@
 
 namespace dgx
 {
-namespace dev
-{
-__constant__ double c_tab_d[kTabTotal];
-__constant__ float c_tab_f[kTabTotal];
-} // namespace dev
-
 namespace
 {
 
@@ -85,6 +79,8 @@ std::vector<double> build_table(int K)
           acc += t.rf[s][q] * t.Dco[q * K + j];
         o[s * K + j] = acc;
       }
+  o += 2 * K;
+  eo_halves(t.D, K, o, o + c2); // nodal derivative D (basis.cpp:277-278)
   return tab;
 }
 

@@ -1,0 +1,226 @@
+// Face phase of the fused SIPG apply (included by sipg_kernel.cuh).
+#pragma once
+
+namespace dgx
+{
+namespace dev
+{
+
+// Both faces of axis A of every cell in the CTA (runs before the
+// quadrature-point phase, so G still holds the reference gradient):
+//  own traces      value and reference gradient at the face points from the
+//                  collocation fields: u = rf val, g_b = rf G_b along the
+//                  normal (exact: rf extrapolates polynomials of degree < k);
+//  neighbour trace nodal Sf/Df rows of the neighbour's opposite face, then
+//                  two tangential passes: along t1 (S and the nodal
+//                  derivative D on the value layer, S on the normal
+//                  derivative), along t0 (S on all, D on the value) --
+//                  the same algebra as face_eval + face_tangential_derivative
+//                  (operators.cpp:794-858, 766-788) in two passes;
+//  SIPG flux       operators.cpp:977-1003 (interior), 1069-1089 (boundary);
+//  test side       w = rv + sum_t Dco_t^T rg_t on the face
+//                  (face_tangential_integrate, :782-788) and rg_A, stored to
+//                  OUT for the backward pass.
+template <typename Real, int D, int K, int A>
+__device__ __forceinline__ void face_axis_v4(const ApplyParams<Real> &prm, Real *cell, int task,
+                                             bool active, int p)
+{
+  using L = SL<D, K>;
+  using T = TabLayout<K>;
+  constexpr int P = L::P, NQ = L::NQ, FP = L::FP, NL = L::NL, FS = L::FS;
+  const Real *val = cell;
+  const Real *G = cell + L::OFF_G;
+  Real *NB = cell + L::OFF_NB;  // face s: nu (2s), nw (2s+1)
+  Real *DT = cell + L::OFF_DT;  // neighbour d/dt0 (s), d/dt1 (2 + s)
+  Real *OUT = cell + L::OFF_OUT + (2 * A) * 2 * FP; // face s: w (2s), rgn (2s+1)
+  const int fp = fpt<D, K>(p);
+
+  int2 tf[2] = {make_int2(-2, 0), make_int2(-2, 0)};
+  if (active)
+    {
+      tf[0] = prm.task_face[task * 2 * D + 2 * A];
+      tf[1] = prm.task_face[task * 2 * D + 2 * A + 1];
+    }
+  // face geometry at face point p (issued first: longest latency)
+  Real jxw[2], tau[2], jo[2][D], jb[2][D];
+#pragma unroll
+  for (int s = 0; s < 2; ++s)
+    {
+      jxw[s] = tau[s] = Real(0);
+#pragma unroll
+      for (int b = 0; b < D; ++b)
+        jo[s][b] = jb[s][b] = Real(0);
+      if (tf[s].x != -2)
+        {
+          const int fid = tf[s].y & 0x3fffffff;
+          const int side = (tf[s].y >> 30) & 1;
+          const Real *fg = prm.face_geo + (long long)fid * (2 * D + 1) * P + p;
+          jxw[s] = __ldg(fg);
+#pragma unroll
+          for (int b = 0; b < D; ++b)
+            {
+              jo[s][b] = __ldg(fg + (1 + side * D + b) * P);
+              jb[s][b] = __ldg(fg + (1 + (1 - side) * D + b) * P);
+            }
+          tau[s] = __ldg(prm.penalty + fid);
+        }
+    }
+  // neighbour pencils -> nodal value / normal-derivative layer (own low face
+  // meets the neighbour's high face, row index 1, and vice versa)
+#pragma unroll
+  for (int s = 0; s < 2; ++s)
+    {
+      Real nu = Real(0), nw = Real(0);
+      if (tf[s].x >= 0)
+        {
+          const Real *un = prm.u + (long long)tf[s].x * NQ;
+          Real x[K];
+#pragma unroll
+          for (int m = 0; m < K; ++m)
+            x[m] = __ldg(un + gidx<D, K, A>(p, m));
+          if (s == 0)
+            {
+              nu = dot_row<Real, K, T::oSf + K>(x);
+              nw = dot_row<Real, K, T::oDf + K>(x);
+            }
+          else
+            {
+              nu = dot_row<Real, K, T::oSf>(x);
+              nw = dot_row<Real, K, T::oDf>(x);
+            }
+        }
+      NB[(2 * s) * FP + fp] = nu;
+      NB[(2 * s + 1) * FP + fp] = nw;
+    }
+  // own traces from the collocation fields along the normal
+  Real own_u[2], own_g[2][D];
+  {
+    Real x[K];
+    load_pencil<Real, D, K, A>(val, p, x);
+    own_u[0] = dot_row<Real, K, T::oRf>(x);
+    own_u[1] = dot_row<Real, K, T::oRf + K>(x);
+#pragma unroll
+    for (int b = 0; b < D; ++b)
+      {
+        load_pencil<Real, D, K, A>(G + b * FS, p, x);
+        own_g[0][b] = dot_row<Real, K, T::oRf>(x);
+        own_g[1][b] = dot_row<Real, K, T::oRf + K>(x);
+      }
+  }
+  __syncthreads();
+
+  if constexpr (D == 3)
+    {
+      // pass 1, along t1: nu -> (S nu, D nu -> DT[2+s]); nw -> S nw
+      for (int t = p; t < 4 * NL; t += P)
+        {
+          const int f = t / NL, l = t - f * NL;
+          Real a[K], b[K];
+          load_line<Real, D, K, 1>(NB + f * FP, l, a);
+          apply_S<Real, K>(a, b);
+          store_line<Real, D, K, 1>(NB + f * FP, l, b);
+          if ((f & 1) == 0)
+            {
+              apply_Dn<Real, K>(a, b);
+              store_line<Real, D, K, 1>(DT + (2 + f / 2) * FP, l, b);
+            }
+        }
+      __syncthreads();
+      // pass 2, along t0: nu -> (S nu, D nu -> DT[s]); nw, dt1 -> S
+      for (int t = p; t < 6 * NL; t += P)
+        {
+          const int f = t / NL, l = t - f * NL;
+          Real *fld = f < 4 ? NB + f * FP : DT + (2 + (f - 4)) * FP;
+          Real a[K], b[K];
+          load_line<Real, D, K, 0>(fld, l, a);
+          apply_S<Real, K>(a, b);
+          store_line<Real, D, K, 0>(fld, l, b);
+          if (f < 4 && (f & 1) == 0)
+            {
+              apply_Dn<Real, K>(a, b);
+              store_line<Real, D, K, 0>(DT + (f / 2) * FP, l, b);
+            }
+        }
+      __syncthreads();
+    }
+  else
+    {
+      for (int t = p; t < 4; t += P)
+        {
+          Real a[K], b[K];
+          load_line<Real, D, K, 0>(NB + t * FP, 0, a);
+          apply_S<Real, K>(a, b);
+          store_line<Real, D, K, 0>(NB + t * FP, 0, b);
+          if ((t & 1) == 0)
+            {
+              apply_Dn<Real, K>(a, b);
+              store_line<Real, D, K, 0>(DT + (t / 2) * FP, 0, b);
+            }
+        }
+      __syncthreads();
+    }
+
+  // flux at face point p for both faces
+#pragma unroll
+  for (int s = 0; s < 2; ++s)
+    {
+      Real rv = Real(0), g = Real(0);
+      if (tf[s].x != -2)
+        {
+          const int side = (tf[s].y >> 30) & 1;
+          Real dn_own = own_g[s][0] * jo[s][0];
+#pragma unroll
+          for (int b = 1; b < D; ++b)
+            dn_own += own_g[s][b] * jo[s][b];
+          if (tf[s].x == -1)
+            {
+              // mirror principle u+ = -u-, dn+ = dn- (operators.cpp:1069-1089)
+              rv = (own_u[s] * tau[s] * Real(2) - dn_own) * jxw[s];
+              g = -(own_u[s] * jxw[s]);
+            }
+          else
+            {
+              const Real nu = NB[(2 * s) * FP + fp], nw = NB[(2 * s + 1) * FP + fp];
+              Real dn_nb = Real(0);
+#pragma unroll
+              for (int b = 0; b < D; ++b)
+                {
+                  const Real gb = b == A ? nw : DT[(2 * (b < A ? b : b - 1) + s) * FP + fp];
+                  dn_nb += gb * jb[s][b];
+                }
+              // side 0: own = e-, side 1: own = e+ (jump = u- - u+)
+              const Real sgn = side == 0 ? Real(1) : Real(-1);
+              const Real delta = own_u[s] - nu;
+              rv = (delta * tau[s] - sgn * ((dn_own + dn_nb) * Real(0.5))) * jxw[s];
+              g = -(sgn * delta * jxw[s] * Real(0.5));
+            }
+        }
+      OUT[(2 * s) * FP + fp] = rv;
+      OUT[(2 * s + 1) * FP + fp] = g * jo[s][A];
+      // tangential test components into the neighbour-derivative slots
+      // (each thread overwrites only the entries it has just read)
+#pragma unroll
+      for (int t = 0; t < D - 1; ++t)
+        DT[(2 * t + s) * FP + fp] = g * jo[s][t < A ? t : t + 1];
+    }
+  __syncthreads();
+  // w = rv + sum_t Dco_t^T rg_t, one tangential direction at a time
+  for (int t = p; t < 2 * NL; t += P)
+    {
+      const int s = t / NL, l = t - s * NL;
+      line_op<Real, D, K, 0, 3>(OUT + 2 * s * FP, DT + s * FP, l);
+    }
+  if constexpr (D == 3)
+    {
+      __syncthreads();
+      for (int t = p; t < 2 * NL; t += P)
+        {
+          const int s = t / NL, l = t - s * NL;
+          line_op<Real, D, K, 1, 3>(OUT + 2 * s * FP, DT + (2 + s) * FP, l);
+        }
+    }
+  __syncthreads();
+}
+
+} // namespace dev
+} // namespace dgx

@@ -29,6 +29,8 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
+#include "sipg_params.hpp"
+
 namespace dgx
 {
 namespace dev
@@ -55,17 +57,20 @@ struct TabLayout
   static constexpr int oRf = oDf + 2 * K;    // rf[2][K]
   static constexpr int oW = oRf + 2 * K;     // Gauss weights [K]
   static constexpr int oRD = oW + K;         // (rf Dco)[2][K] = (Dco^T rf^T)
-  static constexpr int size = oRD + 2 * K;
+  static constexpr int oDnE = oRD + 2 * K;   // even-odd halves of the nodal D
+  static constexpr int oDnO = oDnE + CE * CE;
+  static constexpr int size = oDnO + CE * CE;
 };
 
-constexpr int tab_size(int K) { return 8 * ((K + 1) / 2) * ((K + 1) / 2) + 2 * K * K + 9 * K; }
+constexpr int tab_size(int K) { return 10 * ((K + 1) / 2) * ((K + 1) / 2) + 2 * K * K + 9 * K; }
 // offset of the table for K (K >= 2) inside the per-precision constant block
 constexpr int tab_offset(int K) { return K <= 2 ? 0 : tab_offset(K - 1) + tab_size(K - 1); }
 constexpr int kMaxK = 11;
 constexpr int kTabTotal = tab_offset(kMaxK + 1);
 
-extern __constant__ double c_tab_d[kTabTotal];
-extern __constant__ float c_tab_f[kTabTotal];
+// Defined here (internal linkage) and used only by sipg.cu.
+static __constant__ double c_tab_d[kTabTotal];
+static __constant__ float c_tab_f[kTabTotal];
 
 template <typename Real>
 __device__ __forceinline__ const Real *tab_base();
@@ -176,6 +181,12 @@ __device__ __forceinline__ void apply_Dt(const Real (&x)[K], Real (&y)[K])
   eo_skew<Real, K, TabLayout<K>::oDtE, TabLayout<K>::oDtO>(x, y);
 }
 
+template <typename Real, int K>
+__device__ __forceinline__ void apply_Dn(const Real (&x)[K], Real (&y)[K])
+{
+  eo_skew<Real, K, TabLayout<K>::oDnE, TabLayout<K>::oDnO>(x, y);
+}
+
 template <typename Real, int K, int OFF>
 __device__ __forceinline__ Real dot_row(const Real (&x)[K])
 {
@@ -206,9 +217,8 @@ struct SL
   static constexpr int OFF_G = FS;                    // D gradient / test fields
   static constexpr int OFF_OUT = (D + 1) * FS;        // 2D faces x (w, rgn)
   static constexpr int OFF_NB = OFF_OUT + 4 * D * FP; // nu_lo, nw_lo, nu_hi, nw_hi
-  static constexpr int OFF_OWN = OFF_NB + 4 * FP;     // ou_lo, ou_hi
-  static constexpr int OFF_DT = OFF_OWN + 2 * FP;     // 4(D-1) derivative fields
-  static constexpr int SM_CELL = OFF_DT + 4 * (D - 1) * FP;
+  static constexpr int OFF_DT = OFF_NB + 4 * FP;      // 2(D-1) derivative fields
+  static constexpr int SM_CELL = OFF_DT + 2 * (D - 1) * FP;
 };
 
 // index of the m-th entry along axis A of pencil p (remaining axes
@@ -256,25 +266,6 @@ __device__ __forceinline__ int fln(int l, int m)
     return l + SL<D, K>::FK * m;
 }
 
-// ---- kernel parameters ---------------------------------------------------
-
-// task_face[t * 2D + phi]: x = neighbour slot, or -1 (boundary face), or -2
-// (face not computed on this rank: its contribution arrives by compress);
-// y = local face record | (own side << 30).
-template <typename Real>
-struct ApplyParams
-{
-  const Real *u;
-  Real *y;
-  const Real *cell_geo; // [geo][D*D+1][NQ] or compressed [geo][D*D+1]
-  const Real *face_geo; // [face][2D+1][P]: JxW_f, n.J^{-T}(e-), n.J^{-T}(e+)
-  const Real *penalty;  // [face]
-  const int *task_slot;
-  const int *task_geo;  // cell geometry record, -1: no cell integral
-  const int2 *task_face;
-  int n_tasks;
-};
-
 template <int D, int K>
 struct KernelShape
 {
@@ -282,10 +273,10 @@ struct KernelShape
   static constexpr int P = L::P;
   static constexpr int NQ = L::NQ;
   static constexpr int SM_CELL = L::SM_CELL;
-  // ~160-256 threads per CTA and <= ~72 KB of fp64 shared memory, so that
+  // ~160-256 threads per CTA and <= 74 KB of fp64 shared memory, so that
   // three CTAs share one SM (228 KB)
   static constexpr int NC_THREADS = (192 / P) > 0 ? 192 / P : 1;
-  static constexpr int NC_SMEM = (72 * 1024 / 8) / SM_CELL > 0 ? (72 * 1024 / 8) / SM_CELL : 1;
+  static constexpr int NC_SMEM = (74 * 1024 / 8) / SM_CELL > 0 ? (74 * 1024 / 8) / SM_CELL : 1;
   static constexpr int NC = NC_THREADS < NC_SMEM ? NC_THREADS : NC_SMEM;
   static constexpr int THREADS = NC * P;
   static constexpr int SMEM_REALS = NC * SM_CELL;
@@ -359,222 +350,6 @@ __device__ __forceinline__ void line_op(Real *x, Real *y, int l)
     }
 }
 
-// ---- faces of one axis -----------------------------------------------------
-
-// Both faces of axis A of every cell in the CTA:
-//  own traces      u and dn/dxi_A from the collocation values (rows rf and
-//                  rf Dco along the normal), tangential derivatives Dco_t u;
-//  neighbour trace nodal Sf/Df rows of the neighbour's opposite face, S
-//                  sweeps and Dco along the face (operators.cpp:794-858,
-//                  766-788);
-//  SIPG flux       operators.cpp:977-1003 (interior), 1069-1089 (boundary);
-//  test side       w = rv + sum_t Dco_t^T rg_t on the face
-//                  (face_tangential_integrate, :782-788) and rg_A, stored to
-//                  OUT for the backward pass.
-template <typename Real, int D, int K, int A>
-__device__ __forceinline__ void face_axis(const ApplyParams<Real> &prm, Real *cell, int task,
-                                          bool active, int p)
-{
-  using L = SL<D, K>;
-  using T = TabLayout<K>;
-  constexpr int P = L::P, NQ = L::NQ, FP = L::FP, NL = L::NL;
-  const Real *val = cell;
-  Real *NB = cell + L::OFF_NB;
-  Real *OW = cell + L::OFF_OWN;
-  Real *DT = cell + L::OFF_DT; // nb_t0 lo,hi | nb_t1 lo,hi | own_t0 lo,hi | own_t1 lo,hi
-  Real *OUT = cell + L::OFF_OUT + (2 * A) * 2 * FP; // face lo: w, rgn | face hi: w, rgn
-  const int fp = fpt<D, K>(p);
-
-  int2 tf[2] = {make_int2(-2, 0), make_int2(-2, 0)};
-  if (active)
-    {
-      tf[0] = prm.task_face[task * 2 * D + 2 * A];
-      tf[1] = prm.task_face[task * 2 * D + 2 * A + 1];
-    }
-  // face geometry of face point p (issued first: longest latency)
-  Real jxw[2], tau[2], jo[2][D], jb[2][D];
-#pragma unroll
-  for (int s = 0; s < 2; ++s)
-    {
-      jxw[s] = tau[s] = Real(0);
-#pragma unroll
-      for (int b = 0; b < D; ++b)
-        jo[s][b] = jb[s][b] = Real(0);
-      if (tf[s].x != -2)
-        {
-          const int fid = tf[s].y & 0x3fffffff;
-          const int side = (tf[s].y >> 30) & 1;
-          const Real *fg = prm.face_geo + (long long)fid * (2 * D + 1) * P + p;
-          jxw[s] = __ldg(fg);
-#pragma unroll
-          for (int b = 0; b < D; ++b)
-            {
-              jo[s][b] = __ldg(fg + (1 + side * D + b) * P);
-              jb[s][b] = __ldg(fg + (1 + (1 - side) * D + b) * P);
-            }
-          tau[s] = __ldg(prm.penalty + fid);
-        }
-    }
-  // neighbour pencils -> nodal traces (own low face meets the neighbour's
-  // high face, row index 1, and vice versa)
-#pragma unroll
-  for (int s = 0; s < 2; ++s)
-    {
-      Real nu = Real(0), nw = Real(0);
-      if (tf[s].x >= 0)
-        {
-          const Real *un = prm.u + (long long)tf[s].x * NQ;
-          Real x[K];
-#pragma unroll
-          for (int m = 0; m < K; ++m)
-            x[m] = __ldg(un + gidx<D, K, A>(p, m));
-          if (s == 0)
-            {
-              nu = dot_row<Real, K, T::oSf + K>(x);
-              nw = dot_row<Real, K, T::oDf + K>(x);
-            }
-          else
-            {
-              nu = dot_row<Real, K, T::oSf>(x);
-              nw = dot_row<Real, K, T::oDf>(x);
-            }
-        }
-      NB[(2 * s) * FP + fp] = nu;
-      NB[(2 * s + 1) * FP + fp] = nw;
-    }
-  // own traces from the collocation values along the normal
-  Real own_u[2], own_n[2];
-  {
-    Real x[K];
-    load_pencil<Real, D, K, A>(val, p, x);
-    own_u[0] = dot_row<Real, K, T::oRf>(x);
-    own_u[1] = dot_row<Real, K, T::oRf + K>(x);
-    own_n[0] = dot_row<Real, K, T::oRD>(x);
-    own_n[1] = dot_row<Real, K, T::oRD + K>(x);
-    OW[fp] = own_u[0];
-    OW[FP + fp] = own_u[1];
-  }
-  __syncthreads();
-
-  if constexpr (D == 3)
-    {
-      // (a) along t0: S on the 4 neighbour fields; Dco on the 2 own fields
-      for (int t = p; t < 6 * NL; t += P)
-        {
-          const int f = t / NL, l = t - f * NL;
-          if (f < 4)
-            line_op<Real, D, K, 0, 0>(NB + f * FP, nullptr, l);
-          else
-            line_op<Real, D, K, 0, 1>(OW + (f - 4) * FP, DT + (4 + (f - 4)) * FP, l);
-        }
-      __syncthreads();
-      // (b) along t1: S on nw fields; S then Dco on nu fields; Dco on own
-      for (int t = p; t < 6 * NL; t += P)
-        {
-          const int f = t / NL, l = t - f * NL;
-          if (f < 4)
-            {
-              if ((f & 1) == 0) // nu_lo (0), nu_hi (2)
-                line_op<Real, D, K, 1, 2>(NB + f * FP, DT + (2 + f / 2) * FP, l);
-              else
-                line_op<Real, D, K, 1, 0>(NB + f * FP, nullptr, l);
-            }
-          else
-            line_op<Real, D, K, 1, 1>(OW + (f - 4) * FP, DT + (6 + (f - 4)) * FP, l);
-        }
-      __syncthreads();
-      // (c) along t0: Dco on the interpolated neighbour values
-      for (int t = p; t < 2 * NL; t += P)
-        {
-          const int f = t / NL, l = t - f * NL;
-          line_op<Real, D, K, 0, 1>(NB + 2 * f * FP, DT + f * FP, l);
-        }
-      __syncthreads();
-    }
-  else
-    {
-      for (int t = p; t < 6; t += P)
-        {
-          if (t < 4)
-            {
-              if ((t & 1) == 0)
-                line_op<Real, D, K, 0, 2>(NB + t * FP, DT + (t / 2) * FP, 0);
-              else
-                line_op<Real, D, K, 0, 0>(NB + t * FP, nullptr, 0);
-            }
-          else
-            line_op<Real, D, K, 0, 1>(OW + (t - 4) * FP, DT + (2 + (t - 4)) * FP, 0);
-        }
-      __syncthreads();
-    }
-
-  // (d) flux at face point p for both faces
-  constexpr int NT = D - 1; // tangential directions
-#pragma unroll
-  for (int s = 0; s < 2; ++s)
-    {
-      Real rv = Real(0), g = Real(0);
-      if (tf[s].x != -2)
-        {
-          const int side = (tf[s].y >> 30) & 1;
-          // own reference gradient: normal comp own_n, tangential DT own
-          Real dn_own = Real(0);
-#pragma unroll
-          for (int b = 0; b < D; ++b)
-            {
-              const Real gb = b == A ? own_n[s]
-                                     : DT[(2 * NT + 2 * (b < A ? b : b - 1) + s) * FP + fp];
-              dn_own += gb * jo[s][b];
-            }
-          if (tf[s].x == -1)
-            {
-              // mirror principle u+ = -u-, dn+ = dn- (operators.cpp:1069-1089)
-              rv = (own_u[s] * tau[s] * Real(2) - dn_own) * jxw[s];
-              g = -(own_u[s] * jxw[s]);
-            }
-          else
-            {
-              const Real nu = NB[(2 * s) * FP + fp], nw = NB[(2 * s + 1) * FP + fp];
-              Real dn_nb = Real(0);
-#pragma unroll
-              for (int b = 0; b < D; ++b)
-                {
-                  const Real gb = b == A ? nw : DT[(2 * (b < A ? b : b - 1) + s) * FP + fp];
-                  dn_nb += gb * jb[s][b];
-                }
-              // side 0: own = e-, side 1: own = e+ (jump = u- - u+)
-              const Real sgn = side == 0 ? Real(1) : Real(-1);
-              const Real delta = own_u[s] - nu;
-              rv = (delta * tau[s] - sgn * ((dn_own + dn_nb) * Real(0.5))) * jxw[s];
-              g = -(sgn * delta * jxw[s] * Real(0.5));
-            }
-        }
-      OUT[(2 * s) * FP + fp] = rv;
-      OUT[(2 * s + 1) * FP + fp] = g * jo[s][A];
-      // tangential test components into the (now free) neighbour slots
-#pragma unroll
-      for (int t = 0; t < NT; ++t)
-        DT[(2 * t + s) * FP + fp] = g * jo[s][t < A ? t : t + 1];
-    }
-  __syncthreads();
-  // (e) w = rv + sum_t Dco_t^T rg_t, one tangential direction at a time
-  for (int t = p; t < 2 * NL; t += P)
-    {
-      const int s = t / NL, l = t - s * NL;
-      line_op<Real, D, K, 0, 3>(OUT + 2 * s * FP, DT + s * FP, l);
-    }
-  if constexpr (D == 3)
-    {
-      __syncthreads();
-      for (int t = p; t < 2 * NL; t += P)
-        {
-          const int s = t / NL, l = t - s * NL;
-          line_op<Real, D, K, 1, 3>(OUT + 2 * s * FP, DT + (2 + s) * FP, l);
-        }
-    }
-  __syncthreads();
-}
-
 // Backward step along axis A: v (pencil) += rf_s w_s + (Dco^T rf_s) rgn_s
 // for both faces of the axis (the transposed own traces, folded as rank-1
 // updates into the pass that already holds the pencil).
@@ -592,6 +367,14 @@ __device__ __forceinline__ void add_face_terms(const Real *cell, int p, Real (&v
     v[m] += tab<Real, K>(T::oRf + m) * w0 + tab<Real, K>(T::oRf + K + m) * w1 +
             tab<Real, K>(T::oRD + m) * r0 + tab<Real, K>(T::oRD + K + m) * r1;
 }
+
+} // namespace dev
+} // namespace dgx
+#include "sipg_faces.cuh"
+namespace dgx
+{
+namespace dev
+{
 
 template <typename Real, int D, int K, bool COMPRESSED>
 __global__ void __launch_bounds__(KernelShape<D, K>::THREADS, KernelShape<D, K>::MIN_BLOCKS)
@@ -614,6 +397,42 @@ __global__ void __launch_bounds__(KernelShape<D, K>::THREADS, KernelShape<D, K>:
 
   const int slot = active ? prm.task_slot[task] : 0;
   const int geo = active ? prm.task_geo[task] : -1;
+
+  // ---- L2 prefetch of everything this cell reads later: the geometry
+  //      record (read in the quadrature-point phase), its face records and
+  //      the neighbour cells (read in the face phase). Issued now, the HBM
+  //      latency overlaps the forward pass instead of stalling later.
+  if (active)
+    {
+      constexpr int LINE = 128;
+      if (geo >= 0)
+        {
+          const char *gp = reinterpret_cast<const char *>(
+            prm.cell_geo + (long long)geo * (D * D + 1) * (COMPRESSED ? 1 : NQ));
+          constexpr int bytes = (D * D + 1) * (COMPRESSED ? 1 : NQ) * (int)sizeof(Real);
+          for (int off = p * LINE; off < bytes; off += P * LINE)
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(gp + off));
+        }
+#pragma unroll
+      for (int phi = 0; phi < 2 * D; ++phi)
+        {
+          const int2 tf = prm.task_face[task * 2 * D + phi];
+          if (tf.x == -2)
+            continue;
+          const char *fp = reinterpret_cast<const char *>(
+            prm.face_geo + (long long)(tf.y & 0x3fffffff) * (2 * D + 1) * P);
+          constexpr int fbytes = (2 * D + 1) * P * (int)sizeof(Real);
+          for (int off = p * LINE; off < fbytes; off += P * LINE)
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(fp + off));
+          if (tf.x >= 0)
+            {
+              const char *np = reinterpret_cast<const char *>(prm.u + (long long)tf.x * NQ);
+              constexpr int nbytes = NQ * (int)sizeof(Real);
+              for (int off = p * LINE; off < nbytes; off += P * LINE)
+                asm volatile("prefetch.global.L2 [%0];" ::"l"(np + off));
+            }
+        }
+    }
 
   // ---- forward: val = (S x S x S) u, G_b = Dco_b val ----------------------
   {
@@ -657,6 +476,21 @@ __global__ void __launch_bounds__(KernelShape<D, K>::THREADS, KernelShape<D, K>:
   }
   __syncthreads();
 
+  // ---- faces ------------------------------------------------------------
+#ifndef DGX_EXP_NO_FACE
+  face_axis_v4<Real, D, K, 0>(prm, cell, task, active, p);
+  face_axis_v4<Real, D, K, 1>(prm, cell, task, active, p);
+  if constexpr (D == 3)
+    face_axis_v4<Real, D, K, 2>(prm, cell, task, active, p);
+#else
+  {
+    Real *OUT = cell + L::OFF_OUT;
+    for (int i = p; i < 4 * D * L::FP; i += P)
+      OUT[i] = Real(0);
+    __syncthreads();
+  }
+#endif
+
   // ---- quadrature-point operation t = J^{-1} J^{-T} g JxW ------------------
   //      (operators.cpp:669-709); thread p: the points of its pencil along
   //      axis D-1 (coalesced geometry reads, [geo][comp][q] layout)
@@ -697,10 +531,20 @@ __global__ void __launch_bounds__(KernelShape<D, K>::THREADS, KernelShape<D, K>:
             else
               {
                 const Real *cg = prm.cell_geo + (long long)geo * (D * D + 1) * NQ + p + P * m;
+                // read-once stream: evict-first, keep L2 for the reused
+                // neighbour cells and face records
+#ifdef DGX_EXP_NO_GEO
 #pragma unroll
                 for (int c = 0; c < D * D; ++c)
-                  jit[c] = __ldg(cg + c * NQ);
-                jw = __ldg(cg + D * D * NQ);
+                  jit[c] = (c % (D + 1) == 0) ? Real(1) : Real(0);
+                jw = Real(1e-3) * (Real)(geo & 7);
+                (void)cg;
+#else
+#pragma unroll
+                for (int c = 0; c < D * D; ++c)
+                  jit[c] = __ldcs(cg + c * NQ);
+                jw = __ldcs(cg + D * D * NQ);
+#endif
               }
             Real g[D], ph[D];
 #pragma unroll
@@ -736,14 +580,7 @@ __global__ void __launch_bounds__(KernelShape<D, K>::THREADS, KernelShape<D, K>:
           G[b * FS + q] = t[b];
       }
   }
-  // (no barrier: the face phase reads val only, and its first barrier
-  //  orders these G writes before the backward pass)
-
-  // ---- faces ------------------------------------------------------------
-  face_axis<Real, D, K, 0>(prm, cell, task, active, p);
-  face_axis<Real, D, K, 1>(prm, cell, task, active, p);
-  if constexpr (D == 3)
-    face_axis<Real, D, K, 2>(prm, cell, task, active, p);
+  __syncthreads();
 
   // ---- backward: y = (S^T x S^T x S^T)(sum_b Dco_b^T t_b + face terms) ----
   {

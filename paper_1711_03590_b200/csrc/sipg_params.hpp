@@ -1,0 +1,31 @@
+// Parameters of the fused SIPG apply kernel (shared by the host side).
+#pragma once
+
+#include <cuda_runtime.h>
+
+namespace dgx
+{
+namespace dev
+{
+
+// ---- kernel parameters ---------------------------------------------------
+
+// task_face[t * 2D + phi]: x = neighbour slot, or -1 (boundary face), or -2
+// (face not computed on this rank: its contribution arrives by compress);
+// y = local face record | (own side << 30).
+template <typename Real>
+struct ApplyParams
+{
+  const Real *u;
+  Real *y;
+  const Real *cell_geo; // [geo][D*D+1][NQ] or compressed [geo][D*D+1]
+  const Real *face_geo; // [face][2D+1][P]: JxW_f, n.J^{-T}(e-), n.J^{-T}(e+)
+  const Real *penalty;  // [face]
+  const int *task_slot;
+  const int *task_geo;  // cell geometry record, -1: no cell integral
+  const int2 *task_face;
+  int n_tasks;
+};
+
+} // namespace dev
+} // namespace dgx
