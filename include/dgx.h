@@ -182,7 +182,11 @@ dgx_status dgx_apply(dgx_op *op, double *u, double *y, const dgx_hooks *hooks,
 /* fp32 variant (config.precision = 1). */
 dgx_status dgx_apply_f32(dgx_op *op, float *u, float *y, const dgx_hooks *hooks,
                          void *stream);
-/* Host-pointer convenience for single-rank callers: H2D, apply, D2H. */
+/* Host pointers (layout.total_size values each): H2D, apply, D2H. For a
+ * ghosted layout u's ghost region must already hold the neighbour values
+ * (the caller ran its update) and y returns with the contributions to remote
+ * cells in its ghost region (the caller compresses), i.e. the state between
+ * finish_ghost_update and compress of operators.cpp:245-262. */
 dgx_status dgx_apply_host(dgx_op *op, const double *u, double *y);
 
 /* Split phases for external transports (the two loops of

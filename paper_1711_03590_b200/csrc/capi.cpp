@@ -212,7 +212,10 @@ dgx_status dgx_apply_host(dgx_op *op, const double *u, double *y)
     const long long n = o.layout().total_size();
     dgx::DeviceArray<double> du(n), dy(n);
     dgx::cuda_check(cudaMemcpy(du.get(), u, n * 8, cudaMemcpyHostToDevice), "h2d");
-    o.apply(du.get(), dy.get(), nullptr, nullptr, false);
+    // ghosted layouts: the caller has completed the ghost update on the host
+    // side; run both phases and return the ghost contributions in y
+    o.apply_phase(1, du.get(), dy.get(), nullptr, false);
+    o.apply_phase(2, du.get(), dy.get(), nullptr, false);
     dgx::cuda_check(cudaMemcpy(y, dy.get(), n * 8, cudaMemcpyDeviceToHost), "d2h");
   });
 }

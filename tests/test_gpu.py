@@ -287,3 +287,18 @@ def test_full_size_properties(torch, shape):
         A1 = torch.empty_like(u)
         op.apply(one, A1)
         assert float(A1.abs().max()) < 1e-11 * float(Au.abs().max())
+
+
+def test_reference_adapter(torch):
+    """tests/cpp/adapter_test: the reference's own fixtures (SingleRankOp,
+    distributed_apply with GhostExchanger) with dgx_ref::RankOperator swapped
+    in, against dg::RankOperator (rel L_inf <= 1e-12)."""
+    import os
+    import subprocess
+    from conftest import ROOT
+    exe = os.path.join(ROOT, "tests", "cpp", "_build", "adapter_test")
+    if not os.path.exists(exe):
+        pytest.skip("adapter test not built (needs the reference headers)")
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "ALL PASS" in r.stdout
