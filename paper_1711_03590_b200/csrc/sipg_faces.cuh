@@ -219,7 +219,10 @@ __device__ __forceinline__ void face_axis_v4(const ApplyParams<Real> &prm, Real 
           line_op<Real, D, K, 1, 3>(OUT + 2 * s * FP, DT + (2 + s) * FP, l);
         }
     }
-  __syncthreads();
+  // no trailing barrier: the next axis's first step touches only NB and
+  // reads val/G, disjoint from OUT/DT used above, and its own barrier orders
+  // everything after it; the quadrature-point phase that follows the last
+  // axis writes only G and is followed by a barrier before OUT is read
 }
 
 } // namespace dev
