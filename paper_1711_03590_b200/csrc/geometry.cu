@@ -232,7 +232,11 @@ __global__ void face_geometry_kernel(GeometryJob job, GeoConst gc, int *bad)
     if (a != axis)
       tang[nt++] = a;
   const bool boundary = fc.y < 0;
-  double *fg = job.face_geo + f * (2 * d + 1) * nqf;
+  // full records [2d+1][nqf]; Cartesian (compressed) records [2d+1][1] hold
+  // det |J^{-T} e_axis| without the weight (applied on the fly like the
+  // compressed cell records, geometry.hpp:133-143) and the constant normals
+  const int nrf = job.compress ? 1 : nqf;
+  double *fg = job.face_geo + f * (2 * d + 1) * nrf;
   double area = 0.0, abar = 0.0;
   for (int q = 0; q < nqf; ++q)
     {
@@ -270,7 +274,10 @@ __global__ void face_geometry_kernel(GeometryJob job, GeoConst gc, int *bad)
       for (int i = 0; i < d; ++i)
         normal[i] = sign * nvec[i] / nrm;
       const double jxw_f = det * nrm * wqf;
-      fg[q] = jxw_f;
+      if (!job.compress)
+        fg[q] = jxw_f;
+      else if (q == 0)
+        fg[0] = det * nrm;
       area += jxw_f;
       const double a = job.coefficient ? coef_a(xq) : 1.0;
       abar += a;
@@ -303,8 +310,16 @@ __global__ void face_geometry_kernel(GeometryJob job, GeoConst gc, int *bad)
         }
       for (int j = 0; j < d; ++j)
         {
-          fg[(1 + j) * nqf + q] = job.coefficient ? jni[j] * a : jni[j];
-          fg[(1 + d + j) * nqf + q] = job.coefficient ? jne[j] * a : jne[j];
+          if (!job.compress)
+            {
+              fg[(1 + j) * nqf + q] = job.coefficient ? jni[j] * a : jni[j];
+              fg[(1 + d + j) * nqf + q] = job.coefficient ? jne[j] * a : jne[j];
+            }
+          else if (q == 0)
+            {
+              fg[1 + j] = jni[j];
+              fg[1 + d + j] = jne[j];
+            }
         }
     }
   const double p1sq = (double)k * k;

@@ -4,6 +4,7 @@
 #include "sipg_params.hpp"
 
 #include <algorithm>
+#include <cmath>
 #include <cstring>
 
 namespace dgx
@@ -286,19 +287,63 @@ void Operator::build_geometry(const dgx_setup &s, const std::vector<RawFace> &fa
               cg[(c * ncomp + d_ * d_) * nrec + r] = g.jxw[gc * nrec + r];
             }
         }
-      std::vector<double> fg((size_t)nmy * (2 * d_ + 1) * nqf_), pen(nmy);
+      // Cartesian caches: faces compress like the cells (one record, JxW_f
+      // weight applied on the fly); the reference stores them in full, so
+      // check that they are constant per face
+      const long long nrf = compressed_ ? 1 : nqf_;
+      std::vector<double> wqf(nqf_, 1.0);
+      {
+        const Quad1D qg = gauss(k_);
+        for (long long q = 0; q < nqf_; ++q)
+          {
+            long long idx = q;
+            for (int a = 0; a < d_ - 1; ++a)
+              {
+                wqf[q] *= qg.weights[idx % k_];
+                idx /= k_;
+              }
+          }
+      }
+      std::vector<double> fg((size_t)nmy * (2 * d_ + 1) * nrf), pen(nmy);
       for (long long i = 0; i < nmy; ++i)
         {
           const long long f = layout_.my_faces[i];
           for (long long q = 0; q < nqf_; ++q)
             {
-              double *o = fg.data() + i * (2 * d_ + 1) * nqf_ + q;
-              o[0] = g.face_jxw[f * nqf_ + q];
-              for (int b = 0; b < d_; ++b)
+              const double jw = g.face_jxw[f * nqf_ + q];
+              const double *jni = g.face_jni + (f * nqf_ + q) * d_;
+              const double *jne = g.face_jne + (f * nqf_ + q) * d_;
+              if (!compressed_)
                 {
-                  o[(1 + b) * nqf_] = g.face_jni[(f * nqf_ + q) * d_ + b];
-                  o[(1 + d_ + b) * nqf_] = g.face_jne[(f * nqf_ + q) * d_ + b];
+                  double *o = fg.data() + i * (2 * d_ + 1) * nqf_ + q;
+                  o[0] = jw;
+                  for (int b = 0; b < d_; ++b)
+                    {
+                      o[(1 + b) * nqf_] = jni[b];
+                      o[(1 + d_ + b) * nqf_] = jne[b];
+                    }
+                  continue;
                 }
+              double *o = fg.data() + i * (2 * d_ + 1);
+              if (q == 0)
+                {
+                  o[0] = jw / wqf[0];
+                  for (int b = 0; b < d_; ++b)
+                    {
+                      o[1 + b] = jni[b];
+                      o[1 + d_ + b] = jne[b];
+                    }
+                }
+              double scale = 0.0;
+              for (int b = 0; b < d_; ++b)
+                scale = std::max({scale, std::abs(jni[b]), std::abs(jne[b])});
+              bool same = std::abs(jw - o[0] * wqf[q]) <= 1e-12 * std::abs(jw);
+              for (int b = 0; b < d_; ++b)
+                same = same && std::abs(jni[b] - o[1 + b]) <= 1e-12 * scale &&
+                       std::abs(jne[b] - o[1 + d_ + b]) <= 1e-12 * scale;
+              if (!same)
+                fail(Code::invalid_argument,
+                     "geometry: compressed (Cartesian) cache with non-constant face data");
             }
           pen[i] = g.penalty[f];
         }
@@ -359,7 +404,7 @@ void Operator::build_geometry(const dgx_setup &s, const std::vector<RawFace> &fa
       dfl.upload(fl);
       DeviceArray<double> vol(n_slots);
       cell_geo_.resize((size_t)n_owned * ncomp * (compressed_ ? 1 : nq_));
-      face_geo_.resize((size_t)nmy * (2 * d_ + 1) * nqf_);
+      face_geo_.resize((size_t)nmy * (2 * d_ + 1) * (compressed_ ? 1 : nqf_));
       penalty_.resize(nmy);
       GeometryJob job;
       job.d = d_;

@@ -21,9 +21,9 @@ namespace dev
 //  test side       w = rv + sum_t Dco_t^T rg_t on the face
 //                  (face_tangential_integrate, :782-788) and rg_A, stored to
 //                  OUT for the backward pass.
-template <typename Real, int D, int K, int A>
+template <typename Real, int D, int K, int A, bool COMPRESSED>
 __device__ __forceinline__ void face_axis_v4(const ApplyParams<Real> &prm, Real *cell, int task,
-                                             bool active, int p)
+                                             bool active, int p, Real wf)
 {
   using L = SL<D, K>;
   using T = TabLayout<K>;
@@ -54,13 +54,28 @@ __device__ __forceinline__ void face_axis_v4(const ApplyParams<Real> &prm, Real 
         {
           const int fid = tf[s].y & 0x3fffffff;
           const int side = (tf[s].y >> 30) & 1;
-          const Real *fg = prm.face_geo + (long long)fid * (2 * D + 1) * P + p;
-          jxw[s] = __ldg(fg);
-#pragma unroll
-          for (int b = 0; b < D; ++b)
+          if constexpr (COMPRESSED)
             {
-              jo[s][b] = __ldg(fg + (1 + side * D + b) * P);
-              jb[s][b] = __ldg(fg + (1 + (1 - side) * D + b) * P);
+              // Cartesian: one record per face, JxW_f = det |J^{-T} e| w_q
+              const Real *fg = prm.face_geo + (long long)fid * (2 * D + 1);
+              jxw[s] = __ldg(fg) * wf;
+#pragma unroll
+              for (int b = 0; b < D; ++b)
+                {
+                  jo[s][b] = __ldg(fg + 1 + side * D + b);
+                  jb[s][b] = __ldg(fg + 1 + (1 - side) * D + b);
+                }
+            }
+          else
+            {
+              const Real *fg = prm.face_geo + (long long)fid * (2 * D + 1) * P + p;
+              jxw[s] = __ldg(fg);
+#pragma unroll
+              for (int b = 0; b < D; ++b)
+                {
+                  jo[s][b] = __ldg(fg + (1 + side * D + b) * P);
+                  jb[s][b] = __ldg(fg + (1 + (1 - side) * D + b) * P);
+                }
             }
           tau[s] = __ldg(prm.penalty + fid);
         }

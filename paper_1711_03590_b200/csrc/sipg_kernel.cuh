@@ -419,9 +419,10 @@ __global__ void __launch_bounds__(KernelShape<D, K>::THREADS, KernelShape<D, K>:
           const int2 tf = prm.task_face[task * 2 * D + phi];
           if (tf.x == -2)
             continue;
+          constexpr int FREC = COMPRESSED ? 1 : P;
           const char *fp = reinterpret_cast<const char *>(
-            prm.face_geo + (long long)(tf.y & 0x3fffffff) * (2 * D + 1) * P);
-          constexpr int fbytes = (2 * D + 1) * P * (int)sizeof(Real);
+            prm.face_geo + (long long)(tf.y & 0x3fffffff) * (2 * D + 1) * FREC);
+          constexpr int fbytes = (2 * D + 1) * FREC * (int)sizeof(Real);
           for (int off = p * LINE; off < fbytes; off += P * LINE)
             asm volatile("prefetch.global.L2 [%0];" ::"l"(fp + off));
           if (tf.x >= 0)
@@ -478,10 +479,30 @@ __global__ void __launch_bounds__(KernelShape<D, K>::THREADS, KernelShape<D, K>:
 
   // ---- faces ------------------------------------------------------------
 #ifndef DGX_EXP_NO_FACE
-  face_axis_v4<Real, D, K, 0>(prm, cell, task, active, p);
-  face_axis_v4<Real, D, K, 1>(prm, cell, task, active, p);
-  if constexpr (D == 3)
-    face_axis_v4<Real, D, K, 2>(prm, cell, task, active, p);
+  {
+    // tangential quadrature weight of face point p, prod_t w[q_t] in axis
+    // order (wq_face, geometry.cpp:298-308), for compressed face records
+    Real wf = Real(1);
+    if constexpr (COMPRESSED)
+      {
+        int idx = p;
+#pragma unroll
+        for (int t = 0; t < D - 1; ++t)
+          {
+            const int qt = idx % K;
+            idx /= K;
+            Real wa = Real(0);
+#pragma unroll
+            for (int i = 0; i < K; ++i)
+              wa = (qt == i) ? tab<Real, K>(T::oW + i) : wa;
+            wf *= wa;
+          }
+      }
+    face_axis_v4<Real, D, K, 0, COMPRESSED>(prm, cell, task, active, p, wf);
+    face_axis_v4<Real, D, K, 1, COMPRESSED>(prm, cell, task, active, p, wf);
+    if constexpr (D == 3)
+      face_axis_v4<Real, D, K, 2, COMPRESSED>(prm, cell, task, active, p, wf);
+  }
 #else
   {
     Real *OUT = cell + L::OFF_OUT;

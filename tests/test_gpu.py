@@ -137,8 +137,23 @@ def test_device_geometry(torch, name):
     tol = 1e-14 if c.coefficient else 0.0
     assert rel_linf(cg[:, : d * d, :], jit) <= tol
     assert rel_linf(cg[:, d * d, :], jxw) <= tol
-    fg = op.device_geometry(1).reshape(-1, 2 * d + 1, nqf)
     fids = op.device_geometry(3).astype(np.int64)
+    if nrec == 1:
+        # Cartesian: compressed face records, JxW_f = record * prod_t w[q_t]
+        from oracle import oracle as O
+        _, w = O.gauss(k)
+        wqf = np.ones(nqf)
+        for q in range(nqf):
+            idx = q
+            for _a in range(d - 1):
+                wqf[q] *= w[idx % k]
+                idx //= k
+        fr = op.device_geometry(1).reshape(-1, 2 * d + 1, 1)
+        fg = np.concatenate([fr[:, :1, :] * wqf[None, None, :],
+                             np.repeat(fr[:, 1:, :], nqf, axis=2)], axis=1)
+        tol = 1e-15
+    else:
+        fg = op.device_geometry(1).reshape(-1, 2 * d + 1, nqf)
     assert rel_linf(fg[:, 0, :], c.g["geo_face_jxw"].reshape(-1, nqf)[fids]) <= tol
     jni = c.g["geo_face_jni"].reshape(-1, nqf, d)[fids].transpose(0, 2, 1)
     jne = c.g["geo_face_jne"].reshape(-1, nqf, d)[fids].transpose(0, 2, 1)
