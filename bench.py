@@ -62,6 +62,16 @@ def peaks():
         return 6650.0, "fallback"
 
 
+def fp64_peak():
+    """FP64 FMA-pipe peak measured by tools/fp64_pipes.cu (profiles/fp64_peak.json);
+    nominal B200 figure otherwise."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "fp64_peak.json")) as f:
+            return float(json.load(f)["fp64_dfma_tflops"]), "measured (tools/fp64_pipes.cu)"
+    except Exception:
+        return 37.0, "nominal"
+
+
 class ClockSampler:
     """nvidia-smi clocks and throttle reasons sampled during the timed region."""
     Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
@@ -327,12 +337,25 @@ def main():
             traffic = json.load(open(prof)).get("traffic_bytes_per_launch")
         except Exception:
             traffic = None
-    roofline = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
-                "frac": achieved / hbm, "traffic": traffic,
-                "peak_source": hbm_kind, "algorithmic_bytes_per_launch": alg_bytes,
-                "bytes_per_dof": alg_bytes / (lay.owned_size),
-                "launch_ms": launch_ms,
-                "fp64_flops_per_dof_ref_counters": REF_FLOPS_PER_DOF.get(args.config)}
+    # the binding resource: HBM bytes vs FP64 flops (reference counter flops,
+    # SURVEY.md s.8d), whichever takes longer at its peak
+    fpk, fpk_kind = fp64_peak()
+    flops = REF_FLOPS_PER_DOF.get(args.config, 0.0) * lay.owned_size
+    t_hbm = alg_bytes / (hbm * 1e9)
+    t_fp64 = flops / (fpk * 1e12)
+    if t_fp64 > t_hbm and prec == "fp64":
+        achieved_f = flops / (launch_ms * 1e-3) / 1e12
+        roofline = {"bound": "fp64", "achieved": achieved_f, "peak": fpk, "unit": "TFLOP/s",
+                    "frac": achieved_f / fpk, "traffic": traffic, "peak_source": fpk_kind,
+                    "algorithmic_flops_per_launch": flops,
+                    "hbm_achieved_gbs": achieved, "hbm_frac": achieved / hbm}
+    else:
+        roofline = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                    "frac": achieved / hbm, "traffic": traffic, "peak_source": hbm_kind,
+                    "fp64_tflops": flops / (launch_ms * 1e-3) / 1e12}
+    roofline.update({"algorithmic_bytes_per_launch": alg_bytes,
+                     "bytes_per_dof": alg_bytes / (lay.owned_size), "launch_ms": launch_ms,
+                     "fp64_flops_per_dof_ref_counters": REF_FLOPS_PER_DOF.get(args.config)})
 
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
