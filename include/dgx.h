@@ -201,6 +201,24 @@ dgx_status dgx_apply_phase(dgx_op *op, int phase, const void *u, void *y,
 dgx_status dgx_accumulate_plan(dgx_op *op, int idx, const double *contrib,
                                double *y, void *stream);
 
+/* ---- solver around the apply (caller of RankOperator::apply) ------------ */
+
+/* Replaces dg::SolveReport (solvers.hpp:17-22). */
+typedef struct dgx_solve_report
+{
+  int converged;
+  int iterations;
+  double relative_residual;
+} dgx_solve_report;
+
+/* Replaces conjugate_gradient(make_apply(op), b, x, rel_tol, max_iterations)
+ * (solvers.cpp:24-68,189-206) on the device: b, x device pointers of
+ * layout.owned_size values; single-rank operators only (make_apply's
+ * contract, DGX_INVALID_ARGUMENT otherwise); a non-positive p.Ap raises
+ * DGX_RUNTIME_ERROR as the reference does. */
+dgx_status dgx_conjugate_gradient(dgx_op *op, const double *b, double *x, double rel_tol,
+                                  int max_iterations, dgx_solve_report *report, void *stream);
+
 /* ---- native NCCL transport (replaces GhostExchanger, ghost_exchange.hpp:
  * 96-128, over NVLink instead of in-process queues) ---------------------- */
 typedef struct dgx_exchanger dgx_exchanger;

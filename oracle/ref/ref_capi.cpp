@@ -20,6 +20,7 @@
 #include <dg/operators.hpp>
 #include <dg/oracle.hpp>
 #include <dg/quadrature.hpp>
+#include <dg/solvers.hpp>
 
 #include <chrono>
 #include <cstdint>
@@ -490,6 +491,27 @@ int dgref_world_time(void *wp, long long n_applies, double *seconds)
         }
     });
     *seconds = std::chrono::duration<double>(Clock::now() - t0).count();
+  });
+}
+
+// conjugate_gradient(make_apply(op), b, x, tol, maxit) on rank 0 of a
+// single-rank world (solvers.cpp:24-68,189-206); canonical b, x.
+int dgref_world_cg(void *wp, const double *b, double *x, double rel_tol, int max_iterations,
+                   int *converged, int *iterations, double *relative_residual)
+{
+  return guard([&] {
+    World &w = *static_cast<World *>(wp);
+    if (w.ops.size() != 1)
+      throw std::invalid_argument("dgref_world_cg: single-rank worlds only");
+    const long long n = w.ops[0]->layout().owned_size;
+    const std::vector<double> bv(b, b + n);
+    std::vector<double> xv;
+    const SolveReport r = conjugate_gradient(make_apply(*w.ops[0]), bv, xv, rel_tol,
+                                             max_iterations);
+    std::memcpy(x, xv.data(), sizeof(double) * n);
+    *converged = r.converged ? 1 : 0;
+    *iterations = r.iterations;
+    *relative_residual = r.relative_residual;
   });
 }
 

@@ -193,6 +193,17 @@ class World:
         _chk(lib().dgref_world_assemble(self._h, _p(a)))
         return a
 
+    def cg(self, b, rel_tol=1e-10, max_iterations=10000):
+        """conjugate_gradient(make_apply(op), b, x) of the reference."""
+        b = np.ascontiguousarray(b, np.float64)
+        x = np.empty_like(b)
+        conv, its, res = C.c_int(), C.c_int(), C.c_double()
+        _chk(lib().dgref_world_cg(self._h, _p(b), _p(x), C.c_double(rel_tol),
+                                  C.c_int(max_iterations), C.byref(conv), C.byref(its),
+                                  C.byref(res)))
+        return x, dict(converged=bool(conv.value), iterations=its.value,
+                       relative_residual=res.value)
+
     def time(self, n_applies):
         s = C.c_double()
         _chk(lib().dgref_world_time(self._h, C.c_longlong(n_applies),

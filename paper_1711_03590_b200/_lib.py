@@ -98,6 +98,11 @@ class CStats(C.Structure):
                 ("cells_per_cta", C.c_int), ("threads_per_cta", C.c_int)]
 
 
+class CSolveReport(C.Structure):
+    _fields_ = [("converged", C.c_int), ("iterations", C.c_int),
+                ("relative_residual", C.c_double)]
+
+
 _lib = None
 
 # every symbol include/dgx.h declares (checked by the CPU test suite)
@@ -105,7 +110,7 @@ EXPORTS = [
     "dgx_last_error", "dgx_version", "dgx_enumerate_faces", "dgx_partition",
     "dgx_create", "dgx_destroy", "dgx_get_layout", "dgx_get_ghost_cells",
     "dgx_get_plan", "dgx_apply", "dgx_apply_f32", "dgx_apply_host",
-    "dgx_apply_phase", "dgx_accumulate_plan", "dgx_nccl_unique_id",
+    "dgx_apply_phase", "dgx_accumulate_plan", "dgx_conjugate_gradient", "dgx_nccl_unique_id",
     "dgx_exchanger_create", "dgx_exchanger_hooks", "dgx_exchanger_destroy",
     "dgx_get_geometry", "dgx_get_tasks", "dgx_get_stats", "dgx_random_uniform",
 ]

@@ -236,6 +236,17 @@ dgx_status dgx_accumulate_plan(dgx_op *op, int idx, const double *contrib, doubl
   });
 }
 
+dgx_status dgx_conjugate_gradient(dgx_op *op, const double *b, double *x, double rel_tol,
+                                  int max_iterations, dgx_solve_report *report, void *stream)
+{
+  return guard([&] {
+    const dgx_solve_report r = dgx::conjugate_gradient(op_of(op), b, x, rel_tol, max_iterations,
+                                                       static_cast<cudaStream_t>(stream));
+    if (report)
+      *report = r;
+  });
+}
+
 dgx_status dgx_nccl_unique_id(void *id128)
 {
   return guard([&] { dgx::nccl_unique_id(id128); });

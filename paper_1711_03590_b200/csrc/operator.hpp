@@ -73,4 +73,8 @@ private:
   bool recv_contiguous_ = true;
 };
 
+// solvers.cu
+dgx_solve_report conjugate_gradient(Operator &op, const double *b, double *x, double rel_tol,
+                                    int max_iterations, cudaStream_t s);
+
 } // namespace dgx

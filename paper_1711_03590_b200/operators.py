@@ -297,6 +297,17 @@ class RankOperator:
                                    y.ctypes.data_as(C.c_void_p)))
         return y
 
+    def conjugate_gradient(self, b, x, rel_tol=1e-10, max_iterations=10000, stream=None):
+        """conjugate_gradient(make_apply(op), b, x) (solvers.cpp:24-68,189-206)
+        on the device; b, x: CUDA tensors of layout().owned_size values.
+        Returns dict(converged, iterations, relative_residual)."""
+        rep = _lib.CSolveReport()
+        check(lib().dgx_conjugate_gradient(self._h, _ptr(b), _ptr(x), C.c_double(rel_tol),
+                                           C.c_int(max_iterations), C.byref(rep),
+                                           _stream(stream)))
+        return {"converged": bool(rep.converged), "iterations": rep.iterations,
+                "relative_residual": rep.relative_residual}
+
     # -- introspection ------------------------------------------------------
     def plans(self, which):
         """Exchange plans (ghost_exchange.hpp:29-52): list of (neighbor, cells)."""

@@ -317,3 +317,41 @@ def test_reference_adapter(torch):
     r = subprocess.run([exe], capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "ALL PASS" in r.stdout
+
+
+@pytest.mark.parametrize("cfg", [(2, [4, 4], 3, 0.05, 2), (3, [3, 3, 3], 4, 0.05, 2), (3, [4, 4, 4], 2, 0.0, 1)])
+def test_conjugate_gradient_against_reference(torch, cfg):
+    """Device CG (dgx_conjugate_gradient) vs the reference
+    conjugate_gradient(make_apply(op)) (solvers.cpp:24-68,189-206) on the
+    same Dirichlet system: both converge to 1e-10, iteration counts agree to
+    round-off, solutions agree to 1e-8."""
+    from oracle import reflib as R
+    if not R.available():
+        pytest.skip("reference library not built")
+    d, cells, p, amp, m = cfg
+    D = dgx()
+    w = R.World(d, cells, p, amplitude=amp, mapping_degree=m)
+    b = R.random_vector(w.n_dofs, 17)
+    x_ref, rep_ref = w.cg(b, 1e-10, 2000)
+    mesh = D.make_box_mesh(d, cells, amp, False, m)
+    faces = D.enumerate_faces(mesh)
+    part = D.partition_cells(mesh, 1)
+    D.assign_face_owners(mesh, faces, part)
+    op = D.RankOperator(mesh, part, faces, D.Geometry(source="mesh"), D.OperatorConfig(d=d, p=p))
+    bd = torch.tensor(b, device="cuda")
+    xd = torch.empty_like(bd)
+    rep = op.conjugate_gradient(bd, xd, rel_tol=1e-10, max_iterations=2000)
+    assert rep["converged"] and rep_ref["converged"]
+    assert rep["relative_residual"] <= 1e-10
+    assert abs(rep["iterations"] - rep_ref["iterations"]) <= 2, (rep, rep_ref)
+    assert rel_l2(xd.cpu().numpy(), x_ref) < 1e-8
+
+
+def test_conjugate_gradient_contract(torch):
+    D = dgx()
+    c = Case("def3d_p3_m2_r2")
+    op, _ = build(c, rank=0)
+    n = op.layout().owned_size
+    b = torch.ones(n, dtype=torch.float64, device="cuda")
+    with pytest.raises(D.DgxInvalidArgument):  # make_apply: single rank only
+        op.conjugate_gradient(b, torch.empty_like(b))
