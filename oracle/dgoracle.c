@@ -227,6 +227,163 @@ static void gl_nodes(int p, double *nodes)
   dgo_gauss(p + 1, 1, nodes, w);
 }
 
+/* Values and derivatives of the shifted Legendre polynomials P_m(2x-1),
+ * m = 0..n-1, by the three-term recurrence (basis.cpp:40-62). */
+static void shifted_legendre(int n, double x, double *p, double *dp)
+{
+  const double t = 2.0 * x - 1.0;
+  for (int m = 0; m < n; ++m)
+    {
+      if (m == 0)
+        {
+          p[0] = 1.0;
+          dp[0] = 0.0;
+        }
+      else if (m == 1)
+        {
+          p[1] = t;
+          dp[1] = 2.0;
+        }
+      else
+        {
+          p[m] = ((2 * m - 1) * t * p[m - 1] - (m - 1) * p[m - 2]) / m;
+          dp[m] = dp[m - 2] + 2.0 * (2 * m - 1) * p[m - 1];
+        }
+    }
+}
+
+/* One-dimensional basis of make_basis (basis.cpp:116-180): kind 0 Lagrange
+ * in the Gauss-Lobatto points, 1 Lagrange in the Gauss points, 2 Hermite-like
+ * (value/derivative at 0 carried by functions 0/1, derivative/value at 1 by
+ * k-2/k-1, values in k-4 interior Chebyshev points; Legendre coefficients
+ * from the interpolation conditions by Gaussian elimination with partial
+ * pivoting). */
+typedef struct
+{
+  int kind, k;
+  double nodes[64];
+  double coef[32 * 32]; /* hermite: coef[j*k+m] of P_m in function j */
+} basis1d_t;
+
+static int basis_init(basis1d_t *b, int kind, int p)
+{
+  const int k = p + 1;
+  b->kind = kind;
+  b->k = k;
+  if (kind == 0)
+    gl_nodes(p, b->nodes);
+  else if (kind == 1)
+    {
+      double w[64];
+      dgo_gauss(k, 0, b->nodes, w);
+    }
+  else if (kind == 2)
+    {
+      if (p < 3)
+        return fail("make_basis: hermite_like requires cubic or higher degree");
+      if (k > 32)
+        return fail("make_basis: degree too high");
+      double c[32 * 32], a[32 * 32], pv[32], dv[32];
+      for (int m = 0; m < k; ++m)
+        {
+          shifted_legendre(k, 0.0, pv, dv);
+          c[0 * k + m] = pv[m];
+          c[1 * k + m] = dv[m];
+          shifted_legendre(k, 1.0, pv, dv);
+          c[(k - 2) * k + m] = dv[m];
+          c[(k - 1) * k + m] = pv[m];
+          for (int t = 0; t < k - 4; ++t)
+            {
+              const double xi = 0.5 * (1.0 - cos(M_PI * (t + 1) / (k - 3)));
+              shifted_legendre(k, xi, pv, dv);
+              c[(2 + t) * k + m] = pv[m];
+            }
+        }
+      /* a = c^{-1}: Gauss-Jordan with partial pivoting on [c | I] */
+      for (int i = 0; i < k; ++i)
+        for (int j = 0; j < k; ++j)
+          a[i * k + j] = i == j ? 1.0 : 0.0;
+      for (int col = 0; col < k; ++col)
+        {
+          int piv = col;
+          for (int r = col + 1; r < k; ++r)
+            if (fabs(c[r * k + col]) > fabs(c[piv * k + col]))
+              piv = r;
+          for (int j = 0; j < k; ++j)
+            {
+              double t = c[col * k + j];
+              c[col * k + j] = c[piv * k + j];
+              c[piv * k + j] = t;
+              t = a[col * k + j];
+              a[col * k + j] = a[piv * k + j];
+              a[piv * k + j] = t;
+            }
+          const double inv = 1.0 / c[col * k + col];
+          for (int j = 0; j < k; ++j)
+            {
+              c[col * k + j] *= inv;
+              a[col * k + j] *= inv;
+            }
+          for (int r = 0; r < k; ++r)
+            if (r != col && c[r * k + col] != 0.0)
+              {
+                const double f = c[r * k + col];
+                for (int j = 0; j < k; ++j)
+                  {
+                    c[r * k + j] -= f * c[col * k + j];
+                    a[r * k + j] -= f * a[col * k + j];
+                  }
+              }
+        }
+      /* basis function j has the Legendre coefficients of column j */
+      for (int j = 0; j < k; ++j)
+        for (int m = 0; m < k; ++m)
+          b->coef[j * k + m] = a[m * k + j];
+    }
+  else
+    return fail("make_basis: unknown basis kind");
+  return 0;
+}
+
+static void basis_eval(const basis1d_t *b, int j, double x, double *v, double *dv)
+{
+  if (b->kind != 2)
+    {
+      *v = lag_value(b->nodes, b->k, j, x);
+      *dv = lag_derivative(b->nodes, b->k, j, x);
+      return;
+    }
+  double pv[32], pd[32];
+  shifted_legendre(b->k, x, pv, pd);
+  double s = 0.0, sd = 0.0;
+  for (int m = 0; m < b->k; ++m)
+    {
+      s += b->coef[j * b->k + m] * pv[m];
+      sd += b->coef[j * b->k + m] * pd[m];
+    }
+  *v = s;
+  *dv = sd;
+}
+
+/* face rows (basis.cpp:288-309): the Hermite interpolation conditions pin
+ * the value / derivative rows at the end points exactly */
+static void basis_face_rows(const basis1d_t *b, double *vf, double *gf)
+{
+  const int k = b->k;
+  for (int f = 0; f < 2; ++f)
+    for (int j = 0; j < k; ++j)
+      basis_eval(b, j, f ? 1.0 : 0.0, &vf[f * k + j], &gf[f * k + j]);
+  if (b->kind == 2)
+    {
+      for (int i = 0; i < 2 * k; ++i)
+        vf[i] = gf[i] = 0.0;
+      vf[0] = 1.0;
+      gf[1] = 1.0;
+      vf[k + k - 1] = 1.0;
+      gf[k + k - 2] = 1.0;
+    }
+}
+
 /* pack_even_odd + unpack_even_odd (basis.cpp:182-259): the plain matrices
  * are re-expanded from their packed halves (basis.cpp:311-323). */
 static void even_odd_roundtrip(double *m, int rows, int cols, int skew)
@@ -271,34 +428,32 @@ static void even_odd_roundtrip(double *m, int rows, int cols, int skew)
     }
 }
 
-/* shape_matrices, basis.cpp:261-325 (GL basis, l = k Gauss points) */
-int dgo_shape(int p, double *S, double *D, double *Dco, double *Sf, double *Df)
+/* shape_matrices, basis.cpp:261-325 (l = k Gauss points); even-odd
+ * round trip only for the mirror-symmetric bases (basis.cpp:311-323) */
+int dgo_shape(int p, int basis, double *S, double *D, double *Dco, double *Sf, double *Df)
 {
   const int k = p + 1;
-  if (k > 40)
+  if (k > 32)
     return fail("dgo_shape: degree too high");
-  double nodes[64], qp[64], qw[64];
-  gl_nodes(p, nodes);
+  basis1d_t b;
+  if (basis_init(&b, basis, p))
+    return -1;
+  double qp[64], qw[64];
   dgo_gauss(k, 0, qp, qw);
   for (int q = 0; q < k; ++q)
     {
       for (int j = 0; j < k; ++j)
-        {
-          S[q * k + j] = lag_value(nodes, k, j, qp[q]);
-          D[q * k + j] = lag_derivative(nodes, k, j, qp[q]);
-        }
+        basis_eval(&b, j, qp[q], &S[q * k + j], &D[q * k + j]);
       for (int j = 0; j < k; ++j)
         Dco[q * k + j] = lag_derivative(qp, k, j, qp[q]);
     }
-  for (int f = 0; f < 2; ++f)
-    for (int j = 0; j < k; ++j)
-      {
-        Sf[f * k + j] = lag_value(nodes, k, j, f ? 1.0 : 0.0);
-        Df[f * k + j] = lag_derivative(nodes, k, j, f ? 1.0 : 0.0);
-      }
-  even_odd_roundtrip(S, k, k, 0);
-  even_odd_roundtrip(D, k, k, 1);
-  even_odd_roundtrip(Dco, k, k, 1);
+  basis_face_rows(&b, Sf, Df);
+  if (basis != 2)
+    {
+      even_odd_roundtrip(S, k, k, 0);
+      even_odd_roundtrip(D, k, k, 1);
+      even_odd_roundtrip(Dco, k, k, 1);
+    }
   return 0;
 }
 
@@ -939,27 +1094,30 @@ int dgo_apply_rank(int d, int k, int n_cells, int compress,
                    const double *face_jni, const double *face_jne,
                    const double *penalty, int rank, const int *face_owner,
                    int begin, int end, int64_t ng, const uint32_t *ghosts,
-                   const double *u, double *y)
+                   const double *u, double *y, int basis)
 {
   (void)n_cells;
   if (k > 16)
     return fail("dgo_apply_rank: k too large for the table oracle");
-  double nodes[64], qp[64], qw[64];
-  gl_nodes(k - 1, nodes);
+  basis1d_t bas;
+  if (basis_init(&bas, basis, k - 1))
+    return -1;
+  double qp[64], qw[64];
   dgo_gauss(k, 0, qp, qw);
   double v[16 * 16], g[16 * 16], vf[2][16], gf[2][16];
   for (int q = 0; q < k; ++q)
     for (int j = 0; j < k; ++j)
-      {
-        v[q * k + j] = lag_value(nodes, k, j, qp[q]);
-        g[q * k + j] = lag_derivative(nodes, k, j, qp[q]);
-      }
-  for (int f = 0; f < 2; ++f)
-    for (int j = 0; j < k; ++j)
-      {
-        vf[f][j] = lag_value(nodes, k, j, f ? 1.0 : 0.0);
-        gf[f][j] = lag_derivative(nodes, k, j, f ? 1.0 : 0.0);
-      }
+      basis_eval(&bas, j, qp[q], &v[q * k + j], &g[q * k + j]);
+  {
+    double rv[32], rg[32];
+    basis_face_rows(&bas, rv, rg);
+    for (int f = 0; f < 2; ++f)
+      for (int j = 0; j < k; ++j)
+        {
+          vf[f][j] = rv[f * k + j];
+          gf[f][j] = rg[f * k + j];
+        }
+  }
   const int64_t nj = ipow64(k, d), nq = nj, nqf = ipow64(k, d - 1);
   double *wq = malloc(sizeof(double) * nq);
   for (int64_t q = 0; q < nq; ++q)

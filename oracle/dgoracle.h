@@ -29,9 +29,10 @@ int dgo_random_vector(int64_t n, uint32_t seed, double *out);
 /* quadrature.cpp:56-127 */
 int dgo_gauss(int n, int lobatto, double *points, double *weights);
 
-/* GL basis on k = p+1 Gauss points: basis.cpp:116-132,182-325.
+/* Shape matrices on k = p+1 Gauss points: basis.cpp:116-180,182-325.
+ * basis: 0 lagrange_gauss_lobatto, 1 lagrange_gauss, 2 hermite_like.
  * S, D, Dco: k*k row-major (quadrature index = row); Sf, Df: 2*k. */
-int dgo_shape(int p, double *S, double *D, double *Dco, double *Sf,
+int dgo_shape(int p, int basis, double *S, double *D, double *Dco, double *Sf,
               double *Df);
 
 /* enumerate_faces, mesh.cpp:70-132. n_faces first (pass NULL arrays). */
@@ -84,6 +85,7 @@ int dgo_geometry(int d, const int *cells, int m, const double *support,
  *   u, y: rank-local W=1 layout (owned cells then ghost cells, k^d each),
  *   y fully overwritten (ghost slots receive the remote contributions,
  *   i.e. the state before compress, ghost_exchange.cpp:359-398).
+ * basis as for dgo_shape (the reference reads any basis through full tables).
  * Single rank: cell_begin=0, cell_end=n_cells, n_ghost=0, face_owner NULL. */
 int dgo_apply_rank(int d, int k, int n_cells, int compress,
                    const double *inv_jac_t, const double *jxw,
@@ -93,7 +95,8 @@ int dgo_apply_rank(int d, int k, int n_cells, int compress,
                    const double *face_jni, const double *face_jne,
                    const double *penalty, int rank, const int *face_owner,
                    int cell_begin, int cell_end, int64_t n_ghost,
-                   const uint32_t *ghosts, const double *u, double *y);
+                   const uint32_t *ghosts, const double *u, double *y,
+                   int basis);
 
 #ifdef __cplusplus
 }

@@ -64,11 +64,24 @@ def gauss(n, lobatto=False):
     return p, w
 
 
-def shape_matrices(p):
+BASIS = {"lagrange_gauss_lobatto": 0, "gl": 0, "lagrange_gauss": 1, "gauss": 1,
+         "hermite_like": 2, "hermite": 2}
+
+
+def basis_kind(basis, p=None):
+    """BasisKind index; "default" = make_operator_config's Laplacian choice
+    (operators.cpp:27-41)."""
+    if basis == "default":
+        return 2 if p is not None and p >= 3 else 0
+    return BASIS[basis] if isinstance(basis, str) else int(basis)
+
+
+def shape_matrices(p, basis="gl"):
     k = p + 1
     S, D, Dco = (np.empty((k, k)) for _ in range(3))
     Sf, Df = np.empty((2, k)), np.empty((2, k))
-    _chk(lib().dgo_shape(C.c_int(p), _p(S), _p(D), _p(Dco), _p(Sf), _p(Df)))
+    _chk(lib().dgo_shape(C.c_int(p), C.c_int(basis_kind(basis, p)), _p(S), _p(D), _p(Dco),
+                         _p(Sf), _p(Df)))
     return dict(S=S, D=D, Dco=Dco, Sf=Sf, Df=Df)
 
 
@@ -147,7 +160,7 @@ def geometry(d, cells, m, support, k, compress, coefficient, fc):
 
 
 def apply_rank(d, k, n_cells, geom, fc, u, rank=0, face_owner=None,
-               cell_range=None, ghost_cells=None):
+               cell_range=None, ghost_cells=None, basis=0):
     if cell_range is None:
         cell_range = (0, n_cells)
     gh = (np.zeros(0, np.uint32) if ghost_cells is None
@@ -162,12 +175,13 @@ def apply_rank(d, k, n_cells, geom, fc, u, rank=0, face_owner=None,
         _p(fc["exterior"]), _p(fc["fn_int"]), _p(fc["fn_ext"]),
         _p(geom["face_jxw"]), _p(geom["face_jni"]), _p(geom["face_jne"]),
         _p(geom["penalty"]), C.c_int(rank), _p(fo), C.c_int(cell_range[0]),
-        C.c_int(cell_range[1]), C.c_int64(gh.size), _p(gh), _p(u), _p(y)))
+        C.c_int(cell_range[1]), C.c_int64(gh.size), _p(gh), _p(u), _p(y), C.c_int(basis)))
     return y
 
 
 class Problem:
-    """One configuration: box mesh (unit cube), GL basis degree p, g3.
+    """One configuration: box mesh (unit cube), basis of degree p (GL unless
+    basis= selects lagrange_gauss / hermite_like / default), g3.
 
     deform: ("reference", amplitude, m) -> Mesh::map_point deformation of the
             reference (mesh.cpp:11-26); ("vertex", eps) -> BASELINE vertex
@@ -175,8 +189,9 @@ class Problem:
     """
 
     def __init__(self, d, cells, p, periodic=False, deform=None,
-                 coefficient=False, n_ranks=1):
+                 coefficient=False, n_ranks=1, basis="gl"):
         self.d, self.p, self.k = d, p, p + 1
+        self.basis = basis_kind(basis, p)
         self.cells = list(cells)[:d]
         self.n_cells = int(np.prod(self.cells))
         self.periodic = periodic
@@ -203,7 +218,8 @@ class Problem:
         self.n_dofs = self.n_cells * self.dofs_per_cell
 
     def apply(self, x):
-        return apply_rank(self.d, self.k, self.n_cells, self.geom, self.fc, x)
+        return apply_rank(self.d, self.k, self.n_cells, self.geom, self.fc, x,
+                          basis=self.basis)
 
     def rank_ghosts(self, rank):
         return ghosts(rank, self.fc, self.face_owner, self.cell_owner)
@@ -213,4 +229,4 @@ class Problem:
         return apply_rank(self.d, self.k, self.n_cells, self.geom, self.fc,
                           u_local, rank=rank, face_owner=self.face_owner,
                           cell_range=(int(b), int(e)),
-                          ghost_cells=self.rank_ghosts(rank))
+                          ghost_cells=self.rank_ghosts(rank), basis=self.basis)

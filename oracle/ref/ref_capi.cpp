@@ -11,7 +11,10 @@
 //   * SingleRankOp / SerialRanks  (proj/tests/test_operators.cpp:26-39,446-535)
 //   * DistWorld + distributed_apply (proj/tests/test_ghost_exchange.cpp:20-87)
 //   * BenchWorld::run              (proj/src/bench.cpp:104-166)
-// always with the nodal Gauss-Lobatto basis forced.
+// with the nodal Gauss-Lobatto basis forced unless
+// dgref_set_basis selected another BasisKind (or -1: the reference default
+// of make_operator_config, Hermite-like for the Laplacian at p >= 3,
+// operators.cpp:27-41) for the worlds created after it.
 
 #include <dg/basis.hpp>
 #include <dg/geometry.hpp>
@@ -35,6 +38,7 @@ using namespace dg;
 namespace
 {
 thread_local std::string g_err;
+thread_local int g_basis = 0; // BasisKind for new worlds; -1 = reference default
 
 template <typename F>
 int guard(F &&f)
@@ -104,7 +108,8 @@ World *make_world_common(int d, const int *cells, double amplitude,
                        boundary);
   w->cfg = make_operator_config(OperatorKind::laplacian, d, p, W,
                                 GeometryVariant::g3);
-  w->cfg.basis = BasisKind::lagrange_gauss_lobatto; // GL forced (SURVEY s.0)
+  if (g_basis >= 0)
+    w->cfg.basis = static_cast<BasisKind>(g_basis); // GL unless selected
   w->faces = enumerate_faces(w->mesh);
   w->partition = partition_cells(w->mesh, n_ranks);
   assign_face_owners(w->mesh, w->faces, w->partition);
@@ -139,13 +144,28 @@ int dgref_gauss(int n, int lobatto, double *points, double *weights)
   });
 }
 
-// GL-basis shape matrices on k-point Gauss quadrature (basis.cpp:261-325):
+// Basis of the worlds created next: 0 lagrange_gauss_lobatto (default),
+// 1 lagrange_gauss, 2 hermite_like, -1 make_operator_config's choice.
+int dgref_set_basis(int kind)
+{
+  return guard([&] {
+    if (kind < -1 || kind > 2)
+      throw std::invalid_argument("dgref_set_basis: unknown basis kind");
+    g_basis = kind;
+  });
+}
+
+// Shape matrices of the selected basis (dgref_set_basis; -1 resolves as for
+// the Laplacian) on k-point Gauss quadrature (basis.cpp:261-325):
 // S, D (k x k), Dco (k x k), Sf[0..1], Df[0..1] (k each), row-major.
 int dgref_shape_matrices(int p, double *S, double *D, double *Dco,
                          double *Sf, double *Df)
 {
   return guard([&] {
-    const Basis1D b = make_basis(BasisKind::lagrange_gauss_lobatto, p);
+    const BasisKind kind = g_basis >= 0 ? static_cast<BasisKind>(g_basis)
+                           : p >= 3     ? BasisKind::hermite_like
+                                        : BasisKind::lagrange_gauss_lobatto;
+    const Basis1D b = make_basis(kind, p);
     const ShapeMatrices1D sm = shape_matrices(b, gauss_quadrature(p + 1));
     const int k = p + 1;
     std::memcpy(S, sm.S.data(), sizeof(double) * k * k);

@@ -60,7 +60,29 @@ def gauss(n: int, lobatto: bool = False):
     return p, w
 
 
-def shape_matrices(p: int):
+BASIS = {"lagrange_gauss_lobatto": 0, "gl": 0, "lagrange_gauss": 1, "gauss": 1,
+         "hermite_like": 2, "hermite": 2, "default": -1}
+
+
+class _basis:
+    """Select the BasisKind for the worlds / shape matrices made inside."""
+
+    def __init__(self, basis):
+        self.kind = BASIS[basis] if isinstance(basis, str) else int(basis)
+
+    def __enter__(self):
+        _chk(lib().dgref_set_basis(C.c_int(self.kind)))
+
+    def __exit__(self, *exc):
+        lib().dgref_set_basis(C.c_int(0))
+
+
+def shape_matrices(p: int, basis="gl"):
+    with _basis(basis):
+        return _shape_matrices(p)
+
+
+def _shape_matrices(p: int):
     k = p + 1
     S, D, Dco = (np.empty((k, k)) for _ in range(3))
     Sf, Df = np.empty((2, k)), np.empty((2, k))
@@ -79,7 +101,13 @@ class World:
     rank (proj/tests/test_ghost_exchange.cpp:20-50)."""
 
     def __init__(self, d, cells, p, n_ranks=1, amplitude=0.0,
-                 mapping_degree=1, periodic=False, W=1, geometry=None):
+                 mapping_degree=1, periodic=False, W=1, geometry=None, basis="gl"):
+        with _basis(basis):
+            self._create(d, cells, p, n_ranks, amplitude, mapping_degree, periodic, W,
+                         geometry)
+
+    def _create(self, d, cells, p, n_ranks, amplitude, mapping_degree, periodic, W,
+                geometry):
         cells = list(cells) + [1] * (3 - len(cells))
         cc = (C.c_int * 3)(*cells)
         h = C.c_void_p()

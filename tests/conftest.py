@@ -17,7 +17,7 @@ def pytest_configure(config):
 
 def golden_names():
     return sorted(os.path.basename(p)[:-4] for p in glob.glob(os.path.join(GOLDEN, "*.npz"))
-                  if not p.endswith("basics.npz"))
+                  if not os.path.basename(p).startswith("basics"))
 
 
 def load_golden(name):
@@ -41,6 +41,9 @@ class Case:
         self.eps = float(self.g["eps"]) if self.vertex else 0.0
         self.coefficient = bool(self.g["coefficient"]) if self.vertex else False
         self.amplitude = 0.0 if self.vertex else float(self.g["amplitude"])
+        # BasisKind: 0 lagrange_gauss_lobatto, 1 lagrange_gauss, 2 hermite_like
+        self.basis = int(self.g.get("basis", 0))
+        self.basis_name = ("lagrange_gauss_lobatto", "lagrange_gauss", "hermite_like")[self.basis]
         self.seeds = sorted(int(k[1:]) for k in self.g if k.startswith("x") and k[1:].isdigit())
 
     @property

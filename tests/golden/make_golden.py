@@ -17,7 +17,7 @@ Cases follow BASELINE.json's configs at parity-test sizes:
     precompute_geometry on reference meshes) and injected into the
     reference RankOperator.
 
-usage: python tests/golden/make_golden.py
+usage: python tests/golden/make_golden.py [--other-bases]
 """
 import os
 import sys
@@ -33,7 +33,7 @@ GEOM = ["inv_jac_t", "jxw", "face_jxw", "face_jni", "face_jne", "penalty",
         "cell_volume"]
 
 
-def world_arrays(w, n_ranks, prefix=""):
+def world_arrays(w, n_ranks, prefix="", basis="gl"):
     out = {}
     f = w.faces()
     out.update({prefix + "face_" + k: v for k, v in f.items()})
@@ -50,6 +50,11 @@ def world_arrays(w, n_ranks, prefix=""):
                 [p["neighbor"] for p in pl], np.int32)
             for i, p in enumerate(pl):
                 out[f"{prefix}r{r}_{which}{i}_cells"] = p["cells"]
+                if basis != "gl":
+                    # Hermite: two layers per coupled face (ghost_exchange.cpp:49-96)
+                    out[f"{prefix}r{r}_{which}{i}_offsets"] = p["offsets"]
+                    out[f"{prefix}r{r}_{which}{i}_dofs"] = p["dofs"]
+                    continue
                 # GL + first derivatives: whole cells travel
                 dpc = w.dofs_per_cell
                 assert np.array_equal(p["offsets"], np.arange(len(p["cells"]) + 1) * dpc)
@@ -63,17 +68,22 @@ def save(name, **arrays):
     print(f"{name}: {os.path.getsize(path) / 1024:.1f} KiB")
 
 
+BASIS_ID = {"gl": 0, "gauss": 1, "hermite": 2}
+
+
 def reference_case(name, d, cells, p, periodic, amplitude, m, n_ranks, seeds,
-                   dense=False, geometry=True):
+                   dense=False, geometry=True, basis="gl"):
     w = R.World(d, cells, p, n_ranks=n_ranks, amplitude=amplitude,
-                mapping_degree=m, periodic=periodic)
+                mapping_degree=m, periodic=periodic, basis=basis)
     arr = dict(meta=np.array([d, *cells, p, int(periodic), m, n_ranks], np.int64),
                amplitude=np.array(amplitude))
+    if basis != "gl":
+        arr["basis"] = np.array(BASIS_ID[basis])
     for s in seeds:
         x = R.random_vector(w.n_dofs, s)
         arr[f"x{s}"] = x
         arr[f"y{s}"] = w.apply(x)
-    arr.update(world_arrays(w, n_ranks))
+    arr.update(world_arrays(w, n_ranks, basis=basis))
     if geometry:
         for g in GEOM:
             arr["geo_" + g] = w.geometry(g)
@@ -83,20 +93,23 @@ def reference_case(name, d, cells, p, periodic, amplitude, m, n_ranks, seeds,
     save(name, **arr)
 
 
-def injected_case(name, d, cells, p, periodic, eps, coefficient, n_ranks, seeds):
+def injected_case(name, d, cells, p, periodic, eps, coefficient, n_ranks, seeds,
+                  basis="gl"):
     P = O.Problem(d, cells, p, periodic=periodic, deform=("vertex", eps),
                   coefficient=coefficient, n_ranks=n_ranks)
     geo = {k: P.geom[k] for k in ("inv_jac_t", "jxw", "face_jxw", "face_jni",
                                   "face_jne", "penalty")}
     geo["compressed"] = False
-    w = R.World(d, cells, p, n_ranks=n_ranks, periodic=periodic, geometry=geo)
+    w = R.World(d, cells, p, n_ranks=n_ranks, periodic=periodic, geometry=geo, basis=basis)
     arr = dict(meta=np.array([d, *cells, p, int(periodic), 1, n_ranks], np.int64),
                eps=np.array(eps), coefficient=np.array(int(coefficient)))
+    if basis != "gl":
+        arr["basis"] = np.array(BASIS_ID[basis])
     for s in seeds:
         x = R.random_vector(w.n_dofs, s)
         arr[f"x{s}"] = x
         arr[f"y{s}"] = w.apply(x)
-    arr.update(world_arrays(w, n_ranks))
+    arr.update(world_arrays(w, n_ranks, basis=basis))
     for g in GEOM:
         arr["geo_" + g] = P.geom[g]
     save(name, **arr)
@@ -119,7 +132,41 @@ def basics():
     save("basics", **arr)
 
 
+def bases():
+    """Shape matrices of the other two bases (basis.cpp:116-180,261-325)."""
+    arr = {}
+    for p in range(1, 11):
+        for b in ("gauss", "hermite"):
+            if b == "hermite" and p < 3:
+                continue
+            for k, v in R.shape_matrices(p, b).items():
+                arr[f"{b}_p{p}_{k}"] = v
+    save("basics_bases", **arr)
+
+
+def other_bases():
+    """The reference's default Laplacian basis for p >= 3 is Hermite-like
+    (operators.cpp:27-41): 2-layer face reads and exchange plans."""
+    bases()
+    reference_case("herm3d_p3_m2", 3, [3, 3, 3], 3, False, 0.05, 2, 1, [21], basis="hermite")
+    reference_case("herm3d_p5_m2_r3", 3, [3, 3, 4], 5, False, 0.05, 2, 3, [22],
+                   basis="hermite")
+    reference_case("herm2d_p4_m3_r2", 2, [4, 5], 4, False, 0.06, 3, 2, [23], basis="hermite")
+    reference_case("herm3d_periodic_cart_p6_r2", 3, [3, 3, 3], 6, True, 0.0, 1, 2, [24],
+                   basis="hermite")
+    reference_case("herm2d_p10_m2", 2, [3, 3], 10, False, 0.05, 2, 1, [25], basis="hermite")
+    reference_case("herm2d_p3_dense", 2, [2, 3], 3, False, 0.05, 2, 1, [26], dense=True,
+                   basis="hermite")
+    injected_case("herm_c4_vertex_coef_p5_r2", 3, [3, 3, 3], 5, False, 0.1, True, 2, [27],
+                  basis="hermite")
+    reference_case("gauss3d_p3_m2_r2", 3, [3, 2, 2], 3, False, 0.05, 2, 2, [28], basis="gauss")
+    reference_case("gauss2d_p2_periodic", 2, [4, 4], 2, True, 0.0, 1, 1, [29], basis="gauss")
+
+
 def main():
+    if "--other-bases" in sys.argv:
+        other_bases()
+        return
     basics()
     # C1 shape (3D periodic Cartesian, p=3), reduced to 4^3 cells; 2 ranks
     reference_case("c1_periodic_cart_p3", 3, [4, 4, 4], 3, True, 0.0, 1, 1, [0, 11])
@@ -145,3 +192,5 @@ def main():
 
 if __name__ == "__main__":
     main()
+    if "--other-bases" not in sys.argv:
+        other_bases()
