@@ -114,7 +114,10 @@ typedef struct dgx_config
   int d;
   int p;                /* 1..10 */
   int W;                /* accepted for API parity; the layout is W = 1 */
-  int basis;            /* 0: lagrange_gauss_lobatto (others rejected) */
+  int basis;            /* BasisKind (basis.hpp:10-15): 0 lagrange_gauss_lobatto,
+                           1 lagrange_gauss, 2 hermite_like (p >= 3; the
+                           reference default for the Laplacian at p >= 3,
+                           make_operator_config, operators.cpp:27-41) */
   int geometry_variant; /* 3: g3 (others rejected) */
   int precision;        /* 0: fp64, 1: fp32 */
 } dgx_config;
@@ -155,9 +158,15 @@ dgx_status dgx_get_layout(const dgx_op *op, dgx_layout *out);
 /* DoFLayout::ghost_global_cells / ghost_owner (dof_layout.hpp:124-125) */
 dgx_status dgx_get_ghost_cells(const dgx_op *op, uint32_t *cells, int *owners);
 /* ExchangePlan send (which=0) / recv (which=1) neighbour plans
- * (ghost_exchange.hpp:29-52); every planned cell travels whole (k^d dofs). */
+ * (ghost_exchange.hpp:29-52): neighbour and ascending cells. */
 dgx_status dgx_get_plan(const dgx_op *op, int which, int idx, int *n_plans,
                         int *neighbor, int64_t *n_cells, uint32_t *cells);
+/* NeighborPlan::dof_offsets (n_cells + 1) and dofs (cell-local, ascending per
+ * cell) of plan idx (build_exchange_plan, ghost_exchange.cpp:100-144): whole
+ * cells for the nodal / generic bases, the two layers next to every coupled
+ * face for hermite_like. Pass NULL arrays to query n_dofs. */
+dgx_status dgx_get_plan_dofs(const dgx_op *op, int which, int idx, uint32_t *dof_offsets,
+                             int64_t *n_dofs, uint32_t *dofs);
 
 /* Replaces dg::ExchangeHooks (operators.hpp:61-66). Each hook receives the
  * device vector and the stream of the apply; it must leave its work ordered

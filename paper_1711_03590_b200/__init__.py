@@ -6,15 +6,15 @@ kernels for sm_100a. There is no CPU fallback.
 """
 from ._lib import (DgxCudaError, DgxError, DgxInvalidArgument, DgxLogicError,
                    DgxRuntimeError)
-from .operators import (FACE_DTYPE, INVALID_CELL, DoFLayout, Geometry, Mesh,
+from .operators import (BASIS_KINDS, FACE_DTYPE, INVALID_CELL, DoFLayout, Geometry, Mesh,
                         NcclExchanger, OperatorConfig, Partition, RankOperator,
                         assign_face_owners, enumerate_faces, make_box_mesh,
-                        nccl_unique_id, partition_cells, random_vector)
+                        make_operator_config, nccl_unique_id, partition_cells, random_vector)
 
 __all__ = [
     "DgxCudaError", "DgxError", "DgxInvalidArgument", "DgxLogicError",
-    "DgxRuntimeError", "FACE_DTYPE", "INVALID_CELL", "DoFLayout", "Geometry",
+    "DgxRuntimeError", "BASIS_KINDS", "FACE_DTYPE", "INVALID_CELL", "DoFLayout", "Geometry",
     "Mesh", "NcclExchanger", "OperatorConfig", "Partition", "RankOperator",
-    "assign_face_owners", "enumerate_faces", "make_box_mesh", "nccl_unique_id",
+    "assign_face_owners", "enumerate_faces", "make_box_mesh", "make_operator_config", "nccl_unique_id",
     "partition_cells", "random_vector",
 ]

@@ -89,7 +89,10 @@ dgx::Operator &op_of(const dgx_op *op)
 extern "C" {
 
 const char *dgx_last_error(void) { return g_err.c_str(); }
-const char *dgx_version(void) { return "dgx 0.1 (sm_100a, fp64/fp32, GL basis, g3)"; }
+const char *dgx_version(void)
+{
+  return "dgx 0.2 (sm_100a, fp64/fp32, GL / Gauss / Hermite-like bases, g3)";
+}
 
 dgx_status dgx_enumerate_faces(const dgx_mesh *mesh, dgx_raw_face *faces, int64_t *n_faces)
 {
@@ -185,6 +188,24 @@ dgx_status dgx_get_plan(const dgx_op *op, int which, int idx, int *n_plans, int 
       *n_cells = (int64_t)v[idx].cells.size();
     if (cells)
       std::memcpy(cells, v[idx].cells.data(), 4 * v[idx].cells.size());
+  });
+}
+
+dgx_status dgx_get_plan_dofs(const dgx_op *op, int which, int idx, uint32_t *dof_offsets,
+                             int64_t *n_dofs, uint32_t *dofs)
+{
+  return guard([&] {
+    const dgx::RankLayout &l = op_of(op).layout();
+    const auto &v = which == 0 ? l.send : l.recv;
+    if (idx < 0 || idx >= (int)v.size())
+      dgx::fail(dgx::Code::invalid_argument, "dgx_get_plan_dofs: index out of range");
+    const dgx::NeighborPlan &np = v[idx];
+    if (n_dofs)
+      *n_dofs = (int64_t)np.dofs.size();
+    if (dof_offsets)
+      std::memcpy(dof_offsets, np.dof_offsets.data(), 4 * np.dof_offsets.size());
+    if (dofs)
+      std::memcpy(dofs, np.dofs.data(), 4 * np.dofs.size());
   });
 }
 

@@ -88,11 +88,12 @@ template <typename Real>
 struct ApplyParams;
 }
 
-// sipg.cu
-void upload_tables(int K);
+// sipg.cu (kernels in sipg_gl.cu / sipg_gauss.cu / sipg_hermite.cu);
+// basis: 0 lagrange_gauss_lobatto, 1 lagrange_gauss, 2 hermite_like
+void upload_tables(int K, int basis);
 int kernel_cells_per_cta(int D, int K);
 template <typename Real>
-void launch_apply(int D, int K, bool compressed, const dev::ApplyParams<Real> &prm,
+void launch_apply(int D, int K, int basis, bool compressed, const dev::ApplyParams<Real> &prm,
                   cudaStream_t s);
 
 // geometry.cu -- device precompute of the g3 arrays from mapping support
@@ -116,14 +117,18 @@ struct GeometryJob
 };
 void run_geometry(const GeometryJob &job, cudaStream_t s);
 
-// exchange.cu -- halo pack / compress kernels (whole cells: GL basis with
-// first derivatives ships all k^d dofs, ghost_exchange.cpp:49-96).
+// exchange.cu -- halo pack / unpack / compress kernels over the flat value
+// index lists of the exchange plans (slot * k^d + cell-local dof, in plan
+// order: ascending cells, ascending dofs, ghost_exchange.cpp:240-295).
 template <typename T>
-void launch_gather_cells(const T *src, const int *slots, int n_cells, long long nq, T *dst,
-                         cudaStream_t s);
+void launch_gather_values(const T *src, const long long *index, long long n, T *dst,
+                          cudaStream_t s);
 template <typename T>
-void launch_scatter_add_cells(T *dst, const int *slots, int n_cells, long long nq, const T *src,
-                              cudaStream_t s);
+void launch_scatter_values(T *dst, const long long *index, long long n, const T *src,
+                           cudaStream_t s);
+template <typename T>
+void launch_scatter_add_values(T *dst, const long long *index, long long n, const T *src,
+                               cudaStream_t s);
 template <typename Real>
 void launch_convert(const double *src, Real *dst, long long n, cudaStream_t s);
 

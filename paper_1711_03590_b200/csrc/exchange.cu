@@ -1,7 +1,9 @@
-// Halo pack / compress kernels. With the Gauss-Lobatto basis and a face
-// normal derivative the reference ships whole cells (all k^d dofs,
-// ghost_exchange.cpp:49-96), so pack and accumulate are
-// cell-granular gathers: one CTA per cell batch, coalesced over dofs.
+// Halo pack / unpack / compress kernels. The exchange plans list, per
+// neighbour, the cell-local dofs that travel (whole cells for the nodal and
+// generic bases, two layers per coupled face for the Hermite-like basis,
+// ghost_exchange.cpp:46-144); the operator flattens them into value index
+// lists, so pack / unpack / accumulate are plain indexed copies, coalesced
+// over consecutive dofs of a cell.
 #include "device.hpp"
 
 namespace dgx
@@ -9,32 +11,33 @@ namespace dgx
 namespace
 {
 template <typename T>
-__global__ void gather_cells_kernel(const T *__restrict__ src, const int *__restrict__ slots,
-                                    int n_cells, long long nq, T *__restrict__ dst)
+__global__ void gather_values_kernel(const T *__restrict__ src, const long long *__restrict__ index,
+                                     long long n, T *__restrict__ dst)
 {
-  const long long n = (long long)n_cells * nq;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
        i += (long long)gridDim.x * blockDim.x)
-    {
-      const long long c = i / nq, j = i - c * nq;
-      dst[i] = src[(long long)slots[c] * nq + j];
-    }
+    dst[i] = src[index[i]];
 }
 
-// y[slot] += buf, one neighbour at a time: callers launch neighbours in
-// ascending rank order so the accumulation order is fixed
-// (ghost_exchange.cpp:376-395).
 template <typename T>
-__global__ void scatter_add_cells_kernel(T *__restrict__ dst, const int *__restrict__ slots,
-                                         int n_cells, long long nq, const T *__restrict__ src)
+__global__ void scatter_values_kernel(T *__restrict__ dst, const long long *__restrict__ index,
+                                      long long n, const T *__restrict__ src)
 {
-  const long long n = (long long)n_cells * nq;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
        i += (long long)gridDim.x * blockDim.x)
-    {
-      const long long c = i / nq, j = i - c * nq;
-      dst[(long long)slots[c] * nq + j] += src[i];
-    }
+    dst[index[i]] = src[i];
+}
+
+// dst[index] += src for ONE neighbour plan (no repeated index inside a plan);
+// callers launch the plans in ascending neighbour rank so the accumulation
+// order is fixed (ghost_exchange.cpp:376-395).
+template <typename T>
+__global__ void scatter_add_values_kernel(T *__restrict__ dst, const long long *__restrict__ index,
+                                          long long n, const T *__restrict__ src)
+{
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    dst[index[i]] += src[i];
 }
 
 template <typename Real>
@@ -56,25 +59,33 @@ unsigned grid_for(long long n)
 } // namespace
 
 template <typename T>
-void launch_gather_cells(const T *src, const int *slots, int n_cells, long long nq, T *dst,
-                         cudaStream_t s)
+void launch_gather_values(const T *src, const long long *index, long long n, T *dst,
+                          cudaStream_t s)
 {
-  if (n_cells <= 0)
+  if (n <= 0)
     return;
-  gather_cells_kernel<<<grid_for((long long)n_cells * nq), 256, 0, s>>>(src, slots, n_cells,
-                                                                          nq, dst);
-  cuda_check(cudaGetLastError(), "gather_cells");
+  gather_values_kernel<<<grid_for(n), 256, 0, s>>>(src, index, n, dst);
+  cuda_check(cudaGetLastError(), "gather_values");
 }
 
 template <typename T>
-void launch_scatter_add_cells(T *dst, const int *slots, int n_cells, long long nq, const T *src,
-                              cudaStream_t s)
+void launch_scatter_values(T *dst, const long long *index, long long n, const T *src,
+                           cudaStream_t s)
 {
-  if (n_cells <= 0)
+  if (n <= 0)
     return;
-  scatter_add_cells_kernel<<<grid_for((long long)n_cells * nq), 256, 0, s>>>(dst, slots,
-                                                                              n_cells, nq, src);
-  cuda_check(cudaGetLastError(), "scatter_add_cells");
+  scatter_values_kernel<<<grid_for(n), 256, 0, s>>>(dst, index, n, src);
+  cuda_check(cudaGetLastError(), "scatter_values");
+}
+
+template <typename T>
+void launch_scatter_add_values(T *dst, const long long *index, long long n, const T *src,
+                               cudaStream_t s)
+{
+  if (n <= 0)
+    return;
+  scatter_add_values_kernel<<<grid_for(n), 256, 0, s>>>(dst, index, n, src);
+  cuda_check(cudaGetLastError(), "scatter_add_values");
 }
 
 template <typename Real>
@@ -85,14 +96,17 @@ void launch_convert(const double *src, Real *dst, long long n, cudaStream_t s)
   convert_kernel<Real><<<grid_for(n), 256, 0, s>>>(src, dst, n);
   cuda_check(cudaGetLastError(), "convert");
 }
-template void launch_gather_cells<double>(const double *, const int *, int, long long,
-                                         double *, cudaStream_t);
-template void launch_gather_cells<float>(const float *, const int *, int, long long, float *,
-                                        cudaStream_t);
-template void launch_scatter_add_cells<double>(double *, const int *, int, long long,
-                                              const double *, cudaStream_t);
-template void launch_scatter_add_cells<float>(float *, const int *, int, long long,
-                                             const float *, cudaStream_t);
+
+#define DGX_INST(T)                                                                        \
+  template void launch_gather_values<T>(const T *, const long long *, long long, T *,     \
+                                        cudaStream_t);                                    \
+  template void launch_scatter_values<T>(T *, const long long *, long long, const T *,    \
+                                         cudaStream_t);                                   \
+  template void launch_scatter_add_values<T>(T *, const long long *, long long, const T *, \
+                                             cudaStream_t);
+DGX_INST(double)
+DGX_INST(float)
+#undef DGX_INST
 template void launch_convert<float>(const double *, float *, long long, cudaStream_t);
 template void launch_convert<double>(const double *, double *, long long, cudaStream_t);
 

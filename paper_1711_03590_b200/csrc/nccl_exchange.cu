@@ -17,6 +17,7 @@
 #include <dlfcn.h>
 #include <nccl.h>
 
+#include <algorithm>
 #include <cstring>
 #include <mutex>
 
@@ -106,11 +107,12 @@ Exchanger::Exchanger(Operator *op, const void *id128, int n_ranks) : op_(op)
   cuda_check(cudaEventCreateWithFlags(&ev_ready_, cudaEventDisableTiming), "event");
   cuda_check(cudaEventCreateWithFlags(&ev_done_, cudaEventDisableTiming), "event");
   elem_ = op->precision() == 1 ? 4 : 8;
-  const long long n_send = op->send_offsets().back();
-  send_buf_.resize((size_t)n_send * op->nq() * elem_ / 8 + 1);
-  recv_buf_.resize((size_t)n_send * op->nq() * elem_ / 8 + 1);
-  if (!op->recv_contiguous())
-    fail(Code::logic_error, "exchange: receive plans do not follow the ghost storage order");
+  const long long n_send = op->send_offsets().back(), n_recv = op->recv_offsets().back();
+  const long long w = elem_ / 4; // buffers hold doubles; fp32 uses half of them
+  send_buf_.resize((size_t)((n_send * w + 1) / 2 + 1));
+  recv_buf_.resize((size_t)((std::max(n_send, n_recv) * w + 1) / 2 + 1));
+  if (!op->recv_in_place())
+    ghost_buf_.resize((size_t)((n_recv * w + 1) / 2 + 1));
 }
 
 Exchanger::~Exchanger()
@@ -135,41 +137,56 @@ dgx_hooks Exchanger::hooks()
   return h;
 }
 
+namespace
+{
+template <typename F>
+void typed(int elem, F &&f)
+{
+  if (elem == 8)
+    f(double{});
+  else
+    f(float{});
+}
+} // namespace
+
+// update_ghost_values (ghost_exchange.cpp:300-351): pack the plan values,
+// one grouped NCCL send/recv per neighbour on the exchange stream; whole
+// ghost cells land in place in the ghost region, partial (Hermite 2-layer)
+// plans through a buffer and an indexed unpack.
 dgx_status Exchanger::start_update(void *u, cudaStream_t s)
 {
   if (in_flight_)
     fail(Code::logic_error, "update_ghost_values: update already in flight");
   const RankLayout &l = op_->layout();
-  const long long nq = op_->nq();
   const ncclDataType_t dt = elem_ == 4 ? ncclFloat : ncclDouble;
+  const auto &so = op_->send_offsets(), &ro = op_->recv_offsets();
   cuda_check(cudaEventRecord(ev_ready_, s), "event record");
   cuda_check(cudaStreamWaitEvent(comm_stream_, ev_ready_, 0), "wait");
-  const long long n_send = op_->send_offsets().back();
-  if (elem_ == 8)
-    launch_gather_cells<double>(static_cast<const double *>(u), op_->send_slots().get(),
-                                (int)n_send, nq, send_buf_.get(), comm_stream_);
-  else
-    launch_gather_cells<float>(static_cast<const float *>(u), op_->send_slots().get(),
-                               (int)n_send, nq, reinterpret_cast<float *>(send_buf_.get()),
-                               comm_stream_);
+  typed(elem_, [&](auto t) {
+    using T = decltype(t);
+    launch_gather_values<T>(static_cast<const T *>(u), op_->send_index().get(), so.back(),
+                            reinterpret_cast<T *>(send_buf_.get()), comm_stream_);
+  });
   char *ub = static_cast<char *>(u);
   char *sb = reinterpret_cast<char *>(send_buf_.get());
+  char *rb = op_->recv_in_place() ? ub + l.owned_size() * elem_
+                                  : reinterpret_cast<char *>(recv_buf_.get());
   nccl_check(nccl().GroupStart(), "ncclGroupStart");
   for (std::size_t i = 0; i < l.send.size(); ++i)
-    {
-      const long long b = op_->send_offsets()[i], e = op_->send_offsets()[i + 1];
-      nccl_check(nccl().Send(sb + b * nq * elem_, (e - b) * nq, dt, l.send[i].neighbor,
-                             static_cast<ncclComm_t>(comm_), comm_stream_),
-                 "ncclSend");
-    }
+    nccl_check(nccl().Send(sb + so[i] * elem_, so[i + 1] - so[i], dt, l.send[i].neighbor,
+                           static_cast<ncclComm_t>(comm_), comm_stream_),
+               "ncclSend");
   for (std::size_t i = 0; i < l.recv.size(); ++i)
-    {
-      const long long b = op_->recv_offsets()[i], e = op_->recv_offsets()[i + 1];
-      nccl_check(nccl().Recv(ub + (l.owned_size() + b * nq) * elem_, (e - b) * nq, dt,
-                             l.recv[i].neighbor, static_cast<ncclComm_t>(comm_), comm_stream_),
-                 "ncclRecv");
-    }
+    nccl_check(nccl().Recv(rb + ro[i] * elem_, ro[i + 1] - ro[i], dt, l.recv[i].neighbor,
+                           static_cast<ncclComm_t>(comm_), comm_stream_),
+               "ncclRecv");
   nccl_check(nccl().GroupEnd(), "ncclGroupEnd");
+  if (!op_->recv_in_place())
+    typed(elem_, [&](auto t) {
+      using T = decltype(t);
+      launch_scatter_values<T>(static_cast<T *>(u), op_->recv_index().get(), ro.back(),
+                               reinterpret_cast<const T *>(rb), comm_stream_);
+    });
   cuda_check(cudaEventRecord(ev_done_, comm_stream_), "event record");
   in_flight_ = true;
   return DGX_OK;
@@ -184,52 +201,52 @@ dgx_status Exchanger::finish_update(void *, cudaStream_t s)
   return DGX_OK;
 }
 
+// compress (ghost_exchange.cpp:359-398): the ghost contributions travel the
+// reversed update routes; accumulation in ascending neighbour rank, then the
+// ghost region is zeroed.
 dgx_status Exchanger::compress(void *y, cudaStream_t s)
 {
   if (in_flight_)
     {
-      // no ghost-coupled face on this rank: complete the update first
       cuda_check(cudaStreamWaitEvent(s, ev_done_, 0), "wait");
       in_flight_ = false;
     }
   const RankLayout &l = op_->layout();
-  const long long nq = op_->nq();
   const ncclDataType_t dt = elem_ == 4 ? ncclFloat : ncclDouble;
+  const auto &so = op_->send_offsets(), &ro = op_->recv_offsets();
   cuda_check(cudaEventRecord(ev_ready_, s), "event record");
   cuda_check(cudaStreamWaitEvent(comm_stream_, ev_ready_, 0), "wait");
   char *yb = static_cast<char *>(y);
+  char *gb = yb + l.owned_size() * elem_;
+  if (!op_->recv_in_place())
+    {
+      gb = reinterpret_cast<char *>(ghost_buf_.get());
+      typed(elem_, [&](auto t) {
+        using T = decltype(t);
+        launch_gather_values<T>(static_cast<const T *>(y), op_->recv_index().get(), ro.back(),
+                                reinterpret_cast<T *>(gb), comm_stream_);
+      });
+    }
   char *rb = reinterpret_cast<char *>(recv_buf_.get());
   nccl_check(nccl().GroupStart(), "ncclGroupStart");
   for (std::size_t i = 0; i < l.recv.size(); ++i)
-    {
-      const long long b = op_->recv_offsets()[i], e = op_->recv_offsets()[i + 1];
-      nccl_check(nccl().Send(yb + (l.owned_size() + b * nq) * elem_, (e - b) * nq, dt,
-                             l.recv[i].neighbor, static_cast<ncclComm_t>(comm_), comm_stream_),
-                 "ncclSend");
-    }
+    nccl_check(nccl().Send(gb + ro[i] * elem_, ro[i + 1] - ro[i], dt, l.recv[i].neighbor,
+                           static_cast<ncclComm_t>(comm_), comm_stream_),
+               "ncclSend");
   for (std::size_t i = 0; i < l.send.size(); ++i)
-    {
-      const long long b = op_->send_offsets()[i], e = op_->send_offsets()[i + 1];
-      nccl_check(nccl().Recv(rb + b * nq * elem_, (e - b) * nq, dt, l.send[i].neighbor,
-                             static_cast<ncclComm_t>(comm_), comm_stream_),
-                 "ncclRecv");
-    }
+    nccl_check(nccl().Recv(rb + so[i] * elem_, so[i + 1] - so[i], dt, l.send[i].neighbor,
+                           static_cast<ncclComm_t>(comm_), comm_stream_),
+               "ncclRecv");
   nccl_check(nccl().GroupEnd(), "ncclGroupEnd");
   cuda_check(cudaEventRecord(ev_done_, comm_stream_), "event record");
   cuda_check(cudaStreamWaitEvent(s, ev_done_, 0), "wait");
-  // ascending source rank (plans are sorted by neighbour)
   for (std::size_t i = 0; i < l.send.size(); ++i)
-    {
-      const long long b = op_->send_offsets()[i], e = op_->send_offsets()[i + 1];
-      if (elem_ == 8)
-        launch_scatter_add_cells<double>(static_cast<double *>(y), op_->send_slots().get() + b,
-                                         (int)(e - b), nq,
-                                         reinterpret_cast<const double *>(rb + b * nq * 8), s);
-      else
-        launch_scatter_add_cells<float>(static_cast<float *>(y), op_->send_slots().get() + b,
-                                        (int)(e - b), nq,
-                                        reinterpret_cast<const float *>(rb + b * nq * 4), s);
-    }
+    typed(elem_, [&](auto t) {
+      using T = decltype(t);
+      launch_scatter_add_values<T>(static_cast<T *>(y), op_->send_index().get() + so[i],
+                                   so[i + 1] - so[i],
+                                   reinterpret_cast<const T *>(rb) + so[i], s);
+    });
   const long long ghost_vals = l.total_size() - l.owned_size();
   if (ghost_vals > 0)
     cuda_check(cudaMemsetAsync(yb + l.owned_size() * elem_, 0, ghost_vals * elem_, s), "memset");

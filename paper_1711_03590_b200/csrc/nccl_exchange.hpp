@@ -25,7 +25,7 @@ private:
   void *comm_ = nullptr;
   cudaStream_t comm_stream_ = nullptr;
   cudaEvent_t ev_ready_ = nullptr, ev_done_ = nullptr;
-  DeviceArray<double> send_buf_, recv_buf_;
+  DeviceArray<double> send_buf_, recv_buf_, ghost_buf_;
   int elem_ = 8;
   bool in_flight_ = false;
 };

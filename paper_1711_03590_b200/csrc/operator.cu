@@ -35,9 +35,6 @@ MeshDesc to_mesh(const dgx_mesh &m)
 Operator::Operator(const dgx_setup &s, int device) : device_(device)
 {
   const dgx_config &c = s.config;
-  if (c.basis != 0)
-    fail(Code::invalid_argument,
-         "RankOperator: only the nodal Gauss-Lobatto basis is implemented on the device");
   if (c.geometry_variant != 3)
     fail(Code::invalid_argument, "RankOperator: only geometry variant g3 is implemented");
   if (c.d != s.mesh.d)
@@ -52,6 +49,11 @@ Operator::Operator(const dgx_setup &s, int device) : device_(device)
   k_ = c.p + 1;
   if (c.p < 1 || c.p > 10)
     fail(Code::invalid_argument, "RankOperator: supported degrees are 1..10");
+  if (c.basis < 0 || c.basis > 2)
+    fail(Code::invalid_argument, "RankOperator: unknown basis kind");
+  if (c.basis == 2 && c.p < 3)
+    fail(Code::invalid_argument, "RankOperator: the Hermite-type basis needs degree >= 3");
+  basis_ = c.basis;
   precision_ = c.precision;
   nq_ = 1;
   for (int a = 0; a < d_; ++a)
@@ -87,13 +89,13 @@ Operator::Operator(const dgx_setup &s, int device) : device_(device)
   else
     part = make_partition(mesh_, faces, s.n_ranks);
   n_ranks_ = part.n_ranks;
-  layout_ = build_layout(mesh_, faces, part, s.rank, k_);
+  layout_ = build_layout(mesh_, faces, part, s.rank, k_, basis_);
 
   build_tasks(faces, part);
   if (host_only_)
     return;
   build_geometry(s, faces);
-  upload_tables(k_);
+  upload_tables(k_, basis_);
 }
 
 // Task lists. Owned cells whose computed faces never read a ghost form the
@@ -227,31 +229,38 @@ void Operator::build_tasks(const std::vector<RawFace> &faces, const Partition &p
   host_task_geo_ = geo_inner;
   host_task_face_ = tf_inner;
 
-  // exchange plans: owned slots of the cells every neighbour receives
-  std::vector<int> ss;
-  send_offsets_.assign(1, 0);
-  for (const NeighborPlan &np : layout_.send)
-    {
-      for (std::uint32_t c : np.cells)
-        ss.push_back(static_cast<int>(layout_.slot(c)));
-      send_offsets_.push_back((long long)ss.size());
-    }
+  // exchange plans flattened to value indices (plan order: ascending cells,
+  // ascending dofs, pack_plan_values, ghost_exchange.cpp:240-295)
+  auto flatten = [&](const std::vector<NeighborPlan> &plans, std::vector<long long> &idx,
+                     std::vector<long long> &offs) {
+    offs.assign(1, 0);
+    for (const NeighborPlan &np : plans)
+      {
+        for (std::size_t i = 0; i < np.cells.size(); ++i)
+          {
+            const long long sl = layout_.slot(np.cells[i]);
+            if (sl < 0)
+              fail(Code::logic_error, "exchange plan: cell absent from the layout");
+            for (std::uint32_t j = np.dof_offsets[i]; j < np.dof_offsets[i + 1]; ++j)
+              idx.push_back(sl * nq_ + np.dofs[j]);
+          }
+        offs.push_back((long long)idx.size());
+      }
+  };
+  std::vector<long long> si, ri;
+  flatten(layout_.send, si, send_offsets_);
+  flatten(layout_.recv, ri, recv_offsets_);
+  // in place: whole ghost cells, concatenated receive plans = ghost region
+  recv_in_place_ = layout_.whole_cells &&
+                   (long long)ri.size() == (long long)layout_.ghosts.size() * nq_;
+  for (std::size_t i = 0; recv_in_place_ && i < ri.size(); ++i)
+    if (ri[i] != layout_.owned_size() + (long long)i)
+      recv_in_place_ = false;
   if (!host_only_)
-    send_slots_.upload(ss);
-  recv_offsets_.assign(1, 0);
-  long long pos = 0;
-  for (const NeighborPlan &np : layout_.recv)
     {
-      for (std::uint32_t c : np.cells)
-        {
-          if (layout_.slot(c) != n_owned + pos)
-            recv_contiguous_ = false;
-          ++pos;
-        }
-      recv_offsets_.push_back(pos);
+      send_index_.upload(si);
+      recv_index_.upload(ri);
     }
-  if (pos != (long long)layout_.ghosts.size())
-    recv_contiguous_ = false;
 }
 
 void Operator::build_geometry(const dgx_setup &s, const std::vector<RawFace> &faces)
@@ -467,7 +476,8 @@ void Operator::launch_range(int begin, int count, const Real *u, Real *y, cudaSt
   prm.task_geo = task_geo_.get() + begin;
   prm.task_face = task_face_.get() + (long long)begin * 2 * d_;
   prm.n_tasks = count;
-  launch_apply<Real>(d_, k_, compressed_, prm, s);
+  prm.n_owned = static_cast<int>(layout_.n_owned);
+  launch_apply<Real>(d_, k_, basis_, compressed_, prm, s);
 }
 
 void Operator::apply_phase(int phase, const void *u, void *y, cudaStream_t s, bool fp32)
@@ -527,7 +537,7 @@ void Operator::accumulate_plan(int idx, const double *contrib, double *y, cudaSt
   if (idx < 0 || idx >= (int)layout_.send.size())
     fail(Code::invalid_argument, "accumulate_plan: plan index out of range");
   const long long b = send_offsets_[idx], e = send_offsets_[idx + 1];
-  launch_scatter_add_cells(y, send_slots_.get() + b, static_cast<int>(e - b), nq_, contrib, s);
+  launch_scatter_add_values(y, send_index_.get() + b, e - b, contrib, s);
 }
 
 std::vector<double> Operator::geometry(int which) const

@@ -27,6 +27,7 @@ public:
   int d() const { return d_; }
   int k() const { return k_; }
   int precision() const { return precision_; }
+  int basis() const { return basis_; }
   int device() const { return device_; }
   int n_ranks() const { return n_ranks_; }
   long long nq() const { return nq_; }
@@ -41,11 +42,15 @@ public:
   std::vector<double> geometry(int which) const;
   dgx_stats stats() const;
 
-  // send-plan owned slots (device) with per-plan offsets, for the transports
-  const DeviceArray<int> &send_slots() const { return send_slots_; }
+  // exchange plans flattened for the transports: value indices into the
+  // rank-local vector (slot * k^d + dof) in plan order, per-plan offsets in
+  // values (size plans + 1)
+  const DeviceArray<long long> &send_index() const { return send_index_; }
+  const DeviceArray<long long> &recv_index() const { return recv_index_; }
   const std::vector<long long> &send_offsets() const { return send_offsets_; }
   const std::vector<long long> &recv_offsets() const { return recv_offsets_; }
-  bool recv_contiguous() const { return recv_contiguous_; }
+  // whole ghost cells arrive in ghost storage order: receive in place
+  bool recv_in_place() const { return recv_in_place_; }
 
 private:
   void build_tasks(const std::vector<RawFace> &faces, const Partition &part);
@@ -54,7 +59,7 @@ private:
   void launch_range(int begin, int count, const Real *u, Real *y, cudaStream_t s);
 
   MeshDesc mesh_;
-  int d_ = 3, p_ = 1, k_ = 2, precision_ = 0, device_ = 0, n_ranks_ = 1;
+  int d_ = 3, p_ = 1, k_ = 2, precision_ = 0, device_ = 0, n_ranks_ = 1, basis_ = 0;
   long long nq_ = 0, nqf_ = 0;
   RankLayout layout_;
   bool compressed_ = false;
@@ -68,9 +73,9 @@ private:
   DeviceArray<int2> task_face_;
   int n_inner_ = 0, n_coupled_ = 0;
 
-  DeviceArray<int> send_slots_;
-  std::vector<long long> send_offsets_, recv_offsets_; // in cells, size plans+1
-  bool recv_contiguous_ = true;
+  DeviceArray<long long> send_index_, recv_index_;
+  std::vector<long long> send_offsets_, recv_offsets_; // in values, size plans+1
+  bool recv_in_place_ = true;
 };
 
 // solvers.cu

@@ -189,25 +189,145 @@ Quad1D gauss_lobatto(int n)
   return q;
 }
 
-Tables1D make_tables(int p)
+namespace
+{
+// Values and derivatives of the shifted Legendre polynomials P_m(2x-1),
+// m = 0..n-1 (basis.cpp:40-62).
+void shifted_legendre(int n, double x, double *p, double *dp)
+{
+  const double t = 2.0 * x - 1.0;
+  for (int m = 0; m < n; ++m)
+    {
+      if (m == 0)
+        {
+          p[0] = 1.0;
+          dp[0] = 0.0;
+        }
+      else if (m == 1)
+        {
+          p[1] = t;
+          dp[1] = 2.0;
+        }
+      else
+        {
+          p[m] = ((2 * m - 1) * t * p[m - 1] - (m - 1) * p[m - 2]) / m;
+          dp[m] = dp[m - 2] + 2.0 * (2 * m - 1) * p[m - 1];
+        }
+    }
+}
+
+// Legendre coefficients of the Hermite-like basis (basis.cpp:139-177):
+// functions 0/1 carry value/derivative at 0, k-2/k-1 derivative/value at 1,
+// the others interpolate k-4 interior Chebyshev points. Column j of the
+// inverse of the condition matrix (Gauss-Jordan, partial pivoting).
+std::vector<double> hermite_coefficients(int k)
+{
+  std::vector<double> c(k * k), a(k * k, 0.0), pv(k), dv(k);
+  for (int m = 0; m < k; ++m)
+    {
+      shifted_legendre(k, 0.0, pv.data(), dv.data());
+      c[0 * k + m] = pv[m];
+      c[1 * k + m] = dv[m];
+      shifted_legendre(k, 1.0, pv.data(), dv.data());
+      c[(k - 2) * k + m] = dv[m];
+      c[(k - 1) * k + m] = pv[m];
+      for (int t = 0; t < k - 4; ++t)
+        {
+          const double xi = 0.5 * (1.0 - std::cos(M_PI * (t + 1) / (k - 3)));
+          shifted_legendre(k, xi, pv.data(), dv.data());
+          c[(2 + t) * k + m] = pv[m];
+        }
+    }
+  for (int i = 0; i < k; ++i)
+    a[i * k + i] = 1.0;
+  for (int col = 0; col < k; ++col)
+    {
+      int piv = col;
+      for (int r = col + 1; r < k; ++r)
+        if (std::abs(c[r * k + col]) > std::abs(c[piv * k + col]))
+          piv = r;
+      for (int j = 0; j < k; ++j)
+        {
+          std::swap(c[col * k + j], c[piv * k + j]);
+          std::swap(a[col * k + j], a[piv * k + j]);
+        }
+      const double inv = 1.0 / c[col * k + col];
+      for (int j = 0; j < k; ++j)
+        {
+          c[col * k + j] *= inv;
+          a[col * k + j] *= inv;
+        }
+      for (int r = 0; r < k; ++r)
+        if (r != col && c[r * k + col] != 0.0)
+          {
+            const double f = c[r * k + col];
+            for (int j = 0; j < k; ++j)
+              {
+                c[r * k + j] -= f * c[col * k + j];
+                a[r * k + j] -= f * a[col * k + j];
+              }
+          }
+    }
+  std::vector<double> coef(k * k); // coef[j * k + m]: P_m in function j
+  for (int j = 0; j < k; ++j)
+    for (int m = 0; m < k; ++m)
+      coef[j * k + m] = a[m * k + j];
+  return coef;
+}
+} // namespace
+
+int hermite_sign(int k, int j) { return j == k - 2 ? -1 : 1; }
+
+Tables1D make_tables(int p, int basis)
 {
   if (p < 1 || p > 10)
     fail(Code::invalid_argument, "dgx: supported degrees are 1..10");
+  if (basis < 0 || basis > 2)
+    fail(Code::invalid_argument, "RankOperator: unknown basis kind");
+  if (basis == 2 && p < 3)
+    fail(Code::invalid_argument, "RankOperator: the Hermite-type basis needs degree >= 3");
   const int k = p + 1;
-  const std::vector<double> nodes = gauss_lobatto(k).points;
   const Quad1D qg = gauss(k);
   Tables1D t;
   t.k = k;
+  t.basis = basis;
   t.qw = qg.weights;
   t.S.resize(k * k);
   t.Dco.resize(k * k);
   t.D.resize(k * k);
+  // basis function j: value and derivative at x
+  std::vector<double> nodes, coef;
+  if (basis == 0)
+    nodes = gauss_lobatto(k).points;
+  else if (basis == 1)
+    nodes = qg.points;
+  else
+    coef = hermite_coefficients(k);
+  std::vector<double> pv(k), dv(k);
+  auto eval = [&](int j, double x, double &v, double &dvx) {
+    if (basis != 2)
+      {
+        v = lagrange_value(nodes, j, x);
+        dvx = lagrange_derivative(nodes, j, x);
+        return;
+      }
+    // sign-flipped Hermite function psi_j = sigma_j phi_j, sigma_{k-2} = -1:
+    // psi_{k-1-j}(x) = psi_j(1-x), so S, D admit the even-odd form
+    shifted_legendre(k, x, pv.data(), dv.data());
+    double s = 0.0, sd = 0.0;
+    for (int m = 0; m < k; ++m)
+      {
+        s += coef[j * k + m] * pv[m];
+        sd += coef[j * k + m] * dv[m];
+      }
+    v = hermite_sign(k, j) * s;
+    dvx = hermite_sign(k, j) * sd;
+  };
   for (int q = 0; q < k; ++q)
     for (int j = 0; j < k; ++j)
       {
-        t.S[q * k + j] = lagrange_value(nodes, j, qg.points[q]);
+        eval(j, qg.points[q], t.S[q * k + j], t.D[q * k + j]);
         t.Dco[q * k + j] = lagrange_derivative(qg.points, j, qg.points[q]);
-        t.D[q * k + j] = lagrange_derivative(nodes, j, qg.points[q]);
       }
   mirror_roundtrip(t.S, k, false);
   mirror_roundtrip(t.Dco, k, true);
@@ -220,10 +340,20 @@ Tables1D make_tables(int p)
       t.rf[s].resize(k);
       for (int j = 0; j < k; ++j)
         {
-          t.Sf[s][j] = lagrange_value(nodes, j, x);
-          t.Df[s][j] = lagrange_derivative(nodes, j, x);
+          eval(j, x, t.Sf[s][j], t.Df[s][j]);
           t.rf[s][j] = lagrange_value(qg.points, j, x);
         }
+    }
+  if (basis == 2)
+    {
+      // pinned by the interpolation conditions (basis.cpp:298-309), in the
+      // sign-flipped functions
+      for (int s = 0; s < 2; ++s)
+        std::fill(t.Sf[s].begin(), t.Sf[s].end(), 0.0), std::fill(t.Df[s].begin(), t.Df[s].end(), 0.0);
+      t.Sf[0][0] = 1.0;
+      t.Df[0][1] = 1.0;
+      t.Sf[1][k - 1] = 1.0;
+      t.Df[1][k - 2] = hermite_sign(k, k - 2);
     }
   return t;
 }
@@ -404,7 +534,7 @@ long long RankLayout::slot(std::uint32_t g) const
 }
 
 RankLayout build_layout(const MeshDesc &m, const std::vector<RawFace> &faces,
-                        const Partition &p, int rank, int k)
+                        const Partition &p, int rank, int k, int basis)
 {
   if (rank < 0 || rank >= p.n_ranks)
     fail(Code::invalid_argument, "build_dof_layout: rank out of range");
@@ -436,30 +566,64 @@ RankLayout build_layout(const MeshDesc &m, const std::vector<RawFace> &faces,
   for (std::uint32_t c : g)
     l.ghost_owner.push_back(p.cell_owner[c]);
   // exchange plans (ghost_exchange.cpp:100-144): one face side whose cell is
-  // owned elsewhere than the face contributes that cell.
-  std::map<int, std::vector<std::uint32_t>> send, recv;
+  // owned elsewhere than the face contributes that cell, with the dofs the
+  // face evaluation reads (mark_face_dofs, :46-70): two layers next to the
+  // face for the Hermite-like basis, the whole cell otherwise
+  const int nl = basis == 2 ? 2 : 0;
+  auto mark = [&](std::vector<char> &mask, int face_number) {
+    if (mask.empty())
+      mask.assign((size_t)dpc, 0);
+    if (nl == 0)
+      {
+        std::fill(mask.begin(), mask.end(), 1);
+        return;
+      }
+    const int axis = face_number / 2, side = face_number % 2;
+    long long inner = 1;
+    for (int a = 0; a < axis; ++a)
+      inner *= k;
+    for (long long j = 0; j < dpc; ++j)
+      {
+        const int ja = static_cast<int>((j / inner) % k);
+        if (side == 0 ? ja < nl : ja >= k - nl)
+          mask[j] = 1;
+      }
+  };
+  std::map<int, std::map<std::uint32_t, std::vector<char>>> send, recv;
   for (std::size_t fid = 0; fid < faces.size(); ++fid)
     {
       const RawFace &f = faces[fid];
       const int w = p.face_owner[fid];
       const std::uint32_t cells[2] = {f.interior_cell, f.exterior_cell};
+      const int fns[2] = {f.interior_face_number, f.exterior_face_number};
       for (int s = 0; s < (f.at_boundary() ? 1 : 2); ++s)
         {
           const int o = p.cell_owner[cells[s]];
           if (o == w)
             continue;
           if (o == rank)
-            send[w].push_back(cells[s]);
+            mark(send[w][cells[s]], fns[s]);
           else if (w == rank)
-            recv[o].push_back(cells[s]);
+            mark(recv[o][cells[s]], fns[s]);
         }
     }
   for (auto *mp : {&send, &recv})
-    for (auto &[nb, cl] : *mp)
+    for (auto &[nb, cm] : *mp)
       {
-        std::sort(cl.begin(), cl.end());
-        cl.erase(std::unique(cl.begin(), cl.end()), cl.end());
-        (mp == &send ? l.send : l.recv).push_back({nb, cl});
+        NeighborPlan np;
+        np.neighbor = nb;
+        np.dof_offsets.push_back(0);
+        for (auto &[c, mask] : cm)
+          {
+            np.cells.push_back(c);
+            for (long long j = 0; j < dpc; ++j)
+              if (mask[j])
+                np.dofs.push_back(static_cast<std::uint32_t>(j));
+            np.dof_offsets.push_back(static_cast<std::uint32_t>(np.dofs.size()));
+            if (np.dof_offsets.back() - np.dof_offsets[np.dof_offsets.size() - 2] != dpc)
+              l.whole_cells = false;
+          }
+        (mp == &send ? l.send : l.recv).push_back(std::move(np));
       }
   return l;
 }

@@ -50,9 +50,15 @@ Quad1D gauss_lobatto(int n);
 // Tables of the nodal Gauss-Lobatto basis of degree p on k = p+1 Gauss
 // points (basis.cpp:261-325), plus the collocation-space rows the device
 // kernels use for face traces.
+// basis: 0 lagrange_gauss_lobatto, 1 lagrange_gauss, 2 hermite_like
+// (make_basis, basis.cpp:116-180). The Hermite-like functions are stored
+// sign-flipped, psi_j = sigma_j phi_j with sigma_{k-2} = -1 (hermite_sign),
+// which makes S and D mirror-(skew-)symmetric; the kernel multiplies vector
+// entries by the per-dof sign on load and store.
 struct Tables1D
 {
   int k = 0;
+  int basis = 0;
   std::vector<double> S;   // k x k, S[q][j] = phi_j(x_q)
   std::vector<double> Dco; // k x k, collocation derivative in the Gauss points
   std::vector<double> D;   // k x k, D[q][j] = phi_j'(x_q) (nodal derivative)
@@ -62,7 +68,8 @@ struct Tables1D
   std::array<std::vector<double>, 2> rf;
   std::vector<double> qw; // Gauss weights
 };
-Tables1D make_tables(int p);
+Tables1D make_tables(int p, int basis);
+int hermite_sign(int k, int j);
 
 // ------------------------------------------------------------ mesh ------
 
@@ -116,10 +123,18 @@ void assign_face_owners(const std::vector<RawFace> &faces, Partition &p);
 
 // ------------------------------------------------- layout and plans -----
 
+// ExchangePlan::NeighborPlan (ghost_exchange.hpp:29-52): cells ascending,
+// dof_offsets[i]..dof_offsets[i+1] the cell-local dofs of cells[i] that
+// travel (whole cells for the nodal / generic bases with a face normal
+// derivative, two layers per coupled face for the Hermite-like basis,
+// ghost_exchange.cpp:49-144).
 struct NeighborPlan
 {
   int neighbor = -1;
-  std::vector<std::uint32_t> cells; // ascending global ids
+  std::vector<std::uint32_t> cells;
+  std::vector<std::uint32_t> dof_offsets;
+  std::vector<std::uint32_t> dofs;
+  long long n_values() const { return (long long)dofs.size(); }
 };
 
 // Rank-local layout with the reference W=1 numbering (dof_layout.cpp:50-65,
@@ -132,9 +147,8 @@ struct RankLayout
   std::vector<std::uint32_t> ghosts;     // ascending
   std::vector<int> ghost_owner;
   std::vector<std::uint32_t> my_faces;   // face ids computed on this rank
-  // GL + values_and_first_derivatives ships whole cells
-  // (ghost_exchange.cpp:49-144).
   std::vector<NeighborPlan> send, recv;  // ascending neighbour rank
+  bool whole_cells = true;               // every plan ships complete cells
 
   long long owned_size() const { return (long long)n_owned * dofs_per_cell; }
   long long total_size() const
@@ -146,7 +160,7 @@ struct RankLayout
 };
 
 RankLayout build_layout(const MeshDesc &m, const std::vector<RawFace> &faces,
-                        const Partition &p, int rank, int k);
+                        const Partition &p, int rank, int k, int basis);
 
 // Mapping support points [cell][(m+1)^d][d] on Gauss-Lobatto nodes of
 // degree m for the listed global cells (build_mapping, geometry.cpp:36-63,

@@ -1,166 +1,31 @@
-// Constant tables and launch dispatch for the fused SIPG apply kernel.
+// Launch dispatch over the basis kinds (make_basis, basis.cpp:116-180) and
+// the kernel shape query. The kernels and their constant tables live in
+// sipg_gl.cu, sipg_gauss.cu and sipg_hermite.cu (sipg_launch.cuh).
 #include "device.hpp"
-#include "setup.hpp"
 #include "sipg_kernel.cuh"
-
-#include <mutex>
-#include <set>
-#include <tuple>
 
 namespace dgx
 {
-namespace
-{
 
-// Even-odd halves [CE][CE] of a mirror-(skew-)symmetric K x K matrix M
-// (reference basis.cpp:182-221 packing, in the padded layout the device
-// routines eo_sym / eo_skew index).
-void eo_halves(const std::vector<double> &M, int K, double *E, double *O)
-{
-  const int H = K / 2, CE = (K + 1) / 2;
-  for (int q = 0; q < CE; ++q)
-    for (int j = 0; j < CE; ++j)
-      {
-        E[q * CE + j] = j < H ? 0.5 * (M[q * K + j] + M[q * K + (K - 1 - j)])
-                              : M[q * K + j];
-        O[q * CE + j] = j < H ? 0.5 * (M[q * K + j] - M[q * K + (K - 1 - j)]) : 0.0;
-      }
-}
+#define DGX_DECL(B)                                                                       \
+  void upload_tables_##B(int K);                                                         \
+  template <typename Real>                                                               \
+  void launch_apply_##B(int D, int K, bool compressed, const dev::ApplyParams<Real> &prm, \
+                        cudaStream_t s);
+DGX_DECL(gl)
+DGX_DECL(gauss)
+DGX_DECL(hermite)
+#undef DGX_DECL
 
-std::vector<double> transpose(const std::vector<double> &M, int K)
+void upload_tables(int K, int basis)
 {
-  std::vector<double> t(K * K);
-  for (int i = 0; i < K; ++i)
-    for (int j = 0; j < K; ++j)
-      t[i * K + j] = M[j * K + i];
-  return t;
-}
-
-std::vector<double> build_table(int K)
-{
-  const Tables1D t = make_tables(K - 1);
-  const int CE = (K + 1) / 2;
-  std::vector<double> tab(dev::tab_size(K), 0.0);
-  double *b = tab.data();
-  const int c2 = CE * CE;
-  eo_halves(t.S, K, b + 0 * c2, b + 1 * c2);
-  eo_halves(transpose(t.S, K), K, b + 2 * c2, b + 3 * c2);
-  eo_halves(t.Dco, K, b + 4 * c2, b + 5 * c2);
-  eo_halves(transpose(t.Dco, K), K, b + 6 * c2, b + 7 * c2);
-  double *o = b + 8 * c2;
-  for (int i = 0; i < K * K; ++i)
-    o[i] = t.S[i];
-  o += K * K;
-  for (int i = 0; i < K * K; ++i)
-    o[i] = t.Dco[i];
-  o += K * K;
-  for (int s = 0; s < 2; ++s)
-    for (int j = 0; j < K; ++j)
-      o[s * K + j] = t.Sf[s][j];
-  o += 2 * K;
-  for (int s = 0; s < 2; ++s)
-    for (int j = 0; j < K; ++j)
-      o[s * K + j] = t.Df[s][j];
-  o += 2 * K;
-  for (int s = 0; s < 2; ++s)
-    for (int j = 0; j < K; ++j)
-      o[s * K + j] = t.rf[s][j];
-  o += 2 * K;
-  for (int j = 0; j < K; ++j)
-    o[j] = t.qw[j];
-  o += K;
-  // rows (rf_s Dco)[j] = sum_q rf_s[q] Dco[q][j]: own normal-derivative
-  // trace from collocation values, and (Dco^T rf_s^T) for its transpose
-  for (int s = 0; s < 2; ++s)
-    for (int j = 0; j < K; ++j)
-      {
-        double acc = 0.0;
-        for (int q = 0; q < K; ++q)
-          acc += t.rf[s][q] * t.Dco[q * K + j];
-        o[s * K + j] = acc;
-      }
-  o += 2 * K;
-  eo_halves(t.D, K, o, o + c2); // nodal derivative D (basis.cpp:277-278)
-  return tab;
-}
-
-std::mutex g_mutex;
-std::set<std::tuple<int, int>> g_uploaded; // (device, K)
-
-template <typename Real, int D, int K, bool C>
-void launch_one(const dev::ApplyParams<Real> &prm, cudaStream_t s)
-{
-  using KS = dev::KernelShape<D, K>;
-  const size_t smem = (size_t)KS::SMEM_REALS * sizeof(Real);
-  auto kern = dev::sipg_apply_kernel<Real, D, K, C>;
-  static std::set<int> configured;
-  int devid = 0;
-  cuda_check(cudaGetDevice(&devid), "cudaGetDevice");
-  {
-    std::lock_guard<std::mutex> lk(g_mutex);
-    if (!configured.count(devid))
-      {
-        cuda_check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        (int)smem),
-                   "cudaFuncSetAttribute");
-        cuda_check(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
-                                        cudaSharedmemCarveoutMaxShared),
-                   "cudaFuncSetAttribute(carveout)");
-        configured.insert(devid);
-      }
-  }
-  const int grid = (prm.n_tasks + KS::NC - 1) / KS::NC;
-  if (grid > 0)
-    kern<<<grid, KS::THREADS, smem, s>>>(prm);
-  cuda_check(cudaGetLastError(), "sipg_apply_kernel launch");
-}
-
-template <typename Real, int D, int K>
-void launch_k(bool compressed, const dev::ApplyParams<Real> &prm, cudaStream_t s)
-{
-  if (compressed)
-    launch_one<Real, D, K, true>(prm, s);
-  else
-    launch_one<Real, D, K, false>(prm, s);
-}
-
-template <typename Real, int D>
-void launch_d(int K, bool compressed, const dev::ApplyParams<Real> &prm, cudaStream_t s)
-{
-  switch (K)
+  switch (basis)
     {
-    case 2: launch_k<Real, D, 2>(compressed, prm, s); break;
-    case 3: launch_k<Real, D, 3>(compressed, prm, s); break;
-    case 4: launch_k<Real, D, 4>(compressed, prm, s); break;
-    case 5: launch_k<Real, D, 5>(compressed, prm, s); break;
-    case 6: launch_k<Real, D, 6>(compressed, prm, s); break;
-    case 7: launch_k<Real, D, 7>(compressed, prm, s); break;
-    case 8: launch_k<Real, D, 8>(compressed, prm, s); break;
-    case 9: launch_k<Real, D, 9>(compressed, prm, s); break;
-    case 10: launch_k<Real, D, 10>(compressed, prm, s); break;
-    case 11: launch_k<Real, D, 11>(compressed, prm, s); break;
-    default: fail(Code::invalid_argument, "sipg apply: unsupported k");
+    case 0: upload_tables_gl(K); break;
+    case 1: upload_tables_gauss(K); break;
+    case 2: upload_tables_hermite(K); break;
+    default: fail(Code::invalid_argument, "unknown basis kind");
     }
-}
-
-} // namespace
-
-void upload_tables(int K)
-{
-  int devid = 0;
-  cuda_check(cudaGetDevice(&devid), "cudaGetDevice");
-  std::lock_guard<std::mutex> lk(g_mutex);
-  if (g_uploaded.count({devid, K}))
-    return;
-  const std::vector<double> t = build_table(K);
-  std::vector<float> tf(t.begin(), t.end());
-  cuda_check(cudaMemcpyToSymbol(dev::c_tab_d, t.data(), t.size() * sizeof(double),
-                                dev::tab_offset(K) * sizeof(double)),
-             "upload tables");
-  cuda_check(cudaMemcpyToSymbol(dev::c_tab_f, tf.data(), tf.size() * sizeof(float),
-                                dev::tab_offset(K) * sizeof(float)),
-             "upload tables");
-  g_uploaded.insert({devid, K});
 }
 
 int kernel_cells_per_cta(int D, int K)
@@ -177,19 +42,22 @@ int kernel_cells_per_cta(int D, int K)
 }
 
 template <typename Real>
-void launch_apply(int D, int K, bool compressed, const dev::ApplyParams<Real> &prm,
+void launch_apply(int D, int K, int basis, bool compressed, const dev::ApplyParams<Real> &prm,
                   cudaStream_t s)
 {
-  if (D == 2)
-    launch_d<Real, 2>(K, compressed, prm, s);
-  else
-    launch_d<Real, 3>(K, compressed, prm, s);
+  switch (basis)
+    {
+    case 0: launch_apply_gl<Real>(D, K, compressed, prm, s); break;
+    case 1: launch_apply_gauss<Real>(D, K, compressed, prm, s); break;
+    case 2: launch_apply_hermite<Real>(D, K, compressed, prm, s); break;
+    default: fail(Code::invalid_argument, "unknown basis kind");
+    }
 }
 
-template void launch_apply<double>(int, int, bool, const dev::ApplyParams<double> &,
+template void launch_apply<double>(int, int, int, bool, const dev::ApplyParams<double> &,
                                    cudaStream_t);
 #ifdef DGX_WITH_FP32
-template void launch_apply<float>(int, int, bool, const dev::ApplyParams<float> &,
+template void launch_apply<float>(int, int, int, bool, const dev::ApplyParams<float> &,
                                   cudaStream_t);
 #endif
 

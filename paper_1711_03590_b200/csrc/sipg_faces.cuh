@@ -21,9 +21,9 @@ namespace dev
 //  test side       w = rv + sum_t Dco_t^T rg_t on the face
 //                  (face_tangential_integrate, :782-788) and rg_A, stored to
 //                  OUT for the backward pass.
-template <typename Real, int D, int K, int A, bool COMPRESSED>
+template <typename Real, int D, int K, int A, bool COMPRESSED, bool HERM>
 __device__ __forceinline__ void face_axis_v4(const ApplyParams<Real> &prm, Real *cell, int task,
-                                             bool active, int p, Real wf)
+                                             bool active, int p, Real wf, Real sp)
 {
   using L = SL<D, K>;
   using T = TabLayout<K>;
@@ -89,19 +89,33 @@ __device__ __forceinline__ void face_axis_v4(const ApplyParams<Real> &prm, Real 
       if (tf[s].x >= 0)
         {
           const Real *un = prm.u + (long long)tf[s].x * NQ;
-          Real x[K];
-#pragma unroll
-          for (int m = 0; m < K; ++m)
-            x[m] = __ldg(un + gidx<D, K, A>(p, m));
-          if (s == 0)
+          if constexpr (HERM)
             {
-              nu = dot_row<Real, K, T::oSf + K>(x);
-              nw = dot_row<Real, K, T::oDf + K>(x);
+              // two layers: value and derivative live on the edge layer
+              // and its inner neighbour (read_face_dofs, dof_layout.hpp:291-336)
+              const int me = s == 0 ? K - 1 : 0, mi = s == 0 ? K - 2 : 1;
+              const int ro = s == 0 ? K : 0;
+              const Real xe = __ldg(un + gidx<D, K, A>(p, me)) * (sp * hsign<Real, K>(me));
+              const Real xi = __ldg(un + gidx<D, K, A>(p, mi)) * (sp * hsign<Real, K>(mi));
+              nu = tab<Real, K>(T::oSf + ro + me) * xe + tab<Real, K>(T::oSf + ro + mi) * xi;
+              nw = tab<Real, K>(T::oDf + ro + me) * xe + tab<Real, K>(T::oDf + ro + mi) * xi;
             }
           else
             {
-              nu = dot_row<Real, K, T::oSf>(x);
-              nw = dot_row<Real, K, T::oDf>(x);
+              Real x[K];
+#pragma unroll
+              for (int m = 0; m < K; ++m)
+                x[m] = __ldg(un + gidx<D, K, A>(p, m));
+              if (s == 0)
+                {
+                  nu = dot_row<Real, K, T::oSf + K>(x);
+                  nw = dot_row<Real, K, T::oDf + K>(x);
+                }
+              else
+                {
+                  nu = dot_row<Real, K, T::oSf>(x);
+                  nw = dot_row<Real, K, T::oDf>(x);
+                }
             }
         }
       NB[(2 * s) * FP + fp] = nu;

@@ -197,6 +197,42 @@ __device__ __forceinline__ Real dot_row(const Real (&x)[K])
   return s;
 }
 
+// Hermite-like basis, stored sign-flipped (setup.hpp Tables1D): sigma_j.
+template <typename Real, int K>
+__device__ __forceinline__ Real hsign(int j)
+{
+  return j == K - 2 ? Real(-1) : Real(1);
+}
+
+// Dofs of a ghost cell that a face evaluation of the Hermite-like basis may
+// read (two layers next to every face this rank computes for it,
+// read_face_dofs / mark_face_dofs, dof_layout.hpp:291-336,
+// ghost_exchange.cpp:46-70): bit m set if the dof (thread pencil p, index m
+// along axis D-1) is one of them. Ghost data outside these layers is never
+// shipped and must not be read.
+template <int D, int K>
+__device__ __forceinline__ unsigned hermite_ghost_mask(const int2 *tf, int p)
+{
+  constexpr unsigned ALL = (1u << K) - 1u;
+  unsigned keep = 0;
+#pragma unroll
+  for (int phi = 0; phi < 2 * D; ++phi)
+    {
+      if (tf[phi].x == -2)
+        continue;
+      const int a = phi / 2, side = phi % 2;
+      if (a == D - 1)
+        keep |= side == 0 ? 3u : (3u << (K - 2));
+      else
+        {
+          const int c = (D == 2 || a == 0) ? p % K : p / K;
+          if (side == 0 ? c < 2 : c >= K - 2)
+            keep = ALL;
+        }
+    }
+  return keep;
+}
+
 // ---- shared-memory layout -------------------------------------------------
 
 // Volume fields use a padded row stride S1 (odd for even K) so pencils along
@@ -376,10 +412,16 @@ namespace dgx
 namespace dev
 {
 
-template <typename Real, int D, int K, bool COMPRESSED>
+// BASIS 2 (Hermite-like): 2-layer neighbour reads, per-dof sign of the
+// sign-flipped functions, masked ghost cells; otherwise (nodal or generic
+// bases) the neighbour's whole pencil. BASIS is a template argument also so
+// that the instantiations of the per-basis translation units (each with its
+// own constant tables) are distinct kernels, not one weak host stub.
+template <typename Real, int D, int K, bool COMPRESSED, int BASIS>
 __global__ void __launch_bounds__(KernelShape<D, K>::THREADS, KernelShape<D, K>::MIN_BLOCKS)
   sipg_apply_kernel(const ApplyParams<Real> prm)
 {
+  constexpr bool HERM = BASIS == 2;
   using KS = KernelShape<D, K>;
   using L = SL<D, K>;
   using T = TabLayout<K>;
@@ -435,13 +477,35 @@ __global__ void __launch_bounds__(KernelShape<D, K>::THREADS, KernelShape<D, K>:
         }
     }
 
+  // sign of the tangential indices of this thread's pencils (Hermite)
+  Real sp = Real(1);
+  unsigned gmask = (1u << K) - 1u;
+  if constexpr (HERM)
+    {
+      sp = hsign<Real, K>(p % K);
+      if constexpr (D == 3)
+        sp *= hsign<Real, K>(p / K);
+      if (active && slot >= prm.n_owned)
+        {
+          int2 tf[2 * D];
+#pragma unroll
+          for (int phi = 0; phi < 2 * D; ++phi)
+            tf[phi] = prm.task_face[task * 2 * D + phi];
+          gmask = hermite_ghost_mask<D, K>(tf, p);
+        }
+    }
+
   // ---- forward: val = (S x S x S) u, G_b = Dco_b val ----------------------
   {
     Real x[K], z[K];
     const Real *uc = prm.u + (long long)slot * NQ;
 #pragma unroll
     for (int m = 0; m < K; ++m)
-      x[m] = active ? __ldg(uc + p + P * m) : Real(0); // pencil along D-1
+      {
+        x[m] = active ? __ldg(uc + p + P * m) : Real(0); // pencil along D-1
+        if constexpr (HERM)
+          x[m] = ((gmask >> m) & 1u) ? x[m] * (sp * hsign<Real, K>(m)) : Real(0);
+      }
     apply_S<Real, K>(x, z);
     store_pencil<Real, D, K, D - 1>(val, p, z);
     __syncthreads();
@@ -498,10 +562,10 @@ __global__ void __launch_bounds__(KernelShape<D, K>::THREADS, KernelShape<D, K>:
             wf *= wa;
           }
       }
-    face_axis_v4<Real, D, K, 0, COMPRESSED>(prm, cell, task, active, p, wf);
-    face_axis_v4<Real, D, K, 1, COMPRESSED>(prm, cell, task, active, p, wf);
+    face_axis_v4<Real, D, K, 0, COMPRESSED, HERM>(prm, cell, task, active, p, wf, sp);
+    face_axis_v4<Real, D, K, 1, COMPRESSED, HERM>(prm, cell, task, active, p, wf, sp);
     if constexpr (D == 3)
-      face_axis_v4<Real, D, K, 2, COMPRESSED>(prm, cell, task, active, p, wf);
+      face_axis_v4<Real, D, K, 2, COMPRESSED, HERM>(prm, cell, task, active, p, wf, sp);
   }
 #else
   {
@@ -652,7 +716,11 @@ __global__ void __launch_bounds__(KernelShape<D, K>::THREADS, KernelShape<D, K>:
         Real *yc = prm.y + (long long)slot * NQ;
 #pragma unroll
         for (int m = 0; m < K; ++m)
-          yc[p + P * m] = z[m];
+          {
+            if constexpr (HERM)
+              z[m] = ((gmask >> m) & 1u) ? z[m] * (sp * hsign<Real, K>(m)) : Real(0);
+            yc[p + P * m] = z[m];
+          }
       }
   }
 }

@@ -25,6 +25,7 @@ struct ApplyParams
   const int *task_geo;  // cell geometry record, -1: no cell integral
   const int2 *task_face;
   int n_tasks;
+  int n_owned; // slots >= n_owned are ghost cells (ghost-side tasks)
 };
 
 } // namespace dev

@@ -4,9 +4,9 @@ for CPU tensors).
 
 The native C++ transport (`NcclExchanger`, nccl_exchange.cu) is what bench.py
 uses; this module runs the same protocol from Python so that the multi-rank
-logic -- plan order, receive-in-place into the ghost region, compress
-accumulation in ascending source-rank order -- is exercised multi-process on
-CPU (gloo) as well.
+logic -- plan order, whole-cell or two-layer (Hermite-like) plans,
+receive-in-place into the ghost region, compress accumulation in ascending
+source-rank order -- is exercised multi-process on CPU (gloo) as well.
 """
 from __future__ import annotations
 
@@ -17,20 +17,23 @@ import torch.distributed as dist
 class TorchExchanger:
     """update (start/finish) and compress for one rank.
 
-    plans: dict(send=[(neighbor, owned_slots)], recv=[(neighbor, n_cells)])
-    with the reference plan order (ascending neighbour, ascending cells); the
-    receive plans concatenated are the ghost region in storage order.
+    send / recv: [(neighbor, value_index)] in the reference plan order
+    (ascending neighbour, cells ascending, dofs ascending per cell); value
+    indices address the rank-local vector (slot * k^d + dof). Whole-cell
+    receive plans that are contiguous in the ghost region are received in
+    place; partial plans (Hermite-like basis: two layers per coupled face)
+    through a buffer and an indexed unpack.
     """
 
-    def __init__(self, n_owned_cells, dofs_per_cell, send, recv, group=None):
-        self.nq = dofs_per_cell
-        self.n_owned = n_owned_cells
-        self.send = [(nb, torch.as_tensor(slots, dtype=torch.long)) for nb, slots in send]
+    def __init__(self, owned_size, total_size, send, recv, group=None):
+        self.owned_size, self.total_size = owned_size, total_size
+        self.send = [(nb, torch.as_tensor(ix, dtype=torch.long)) for nb, ix in send]
         self.recv = []
-        start = n_owned_cells
-        for nb, n in recv:
-            self.recv.append((nb, start, start + n))
-            start += n
+        for nb, ix in recv:
+            ix = torch.as_tensor(ix, dtype=torch.long)
+            contiguous = len(ix) > 0 and bool(
+                torch.equal(ix, torch.arange(int(ix[0]), int(ix[0]) + len(ix))))
+            self.recv.append((nb, ix, contiguous))
         self.group = group
         self._reqs = None
         self._bufs = None
@@ -38,50 +41,52 @@ class TorchExchanger:
     @classmethod
     def from_operator(cls, op, group=None):
         lay = op.layout()
-        b = lay.owned_cell_begin
-        send = [(nb, cells.astype("int64") - b) for nb, cells in op.plans("send")]
-        recv = [(nb, len(cells)) for nb, cells in op.plans("recv")]
-        return cls(lay.n_owned_cells, lay.dofs_per_cell, send, recv, group)
-
-    def _cells(self, v):
-        return v.view(-1, self.nq)
+        return cls(lay.owned_size, lay.total_size, op.plan_values("send"),
+                   op.plan_values("recv"), group)
 
     # update_ghost_values = start + finish (ghost_exchange.cpp:300-351)
     def start_update(self, u):
         if self._reqs is not None:
             raise RuntimeError("update_ghost_values: update already in flight")
-        cells = self._cells(u)
-        self._bufs, self._reqs = [], []
-        for nb, slots in self.send:
-            buf = cells.index_select(0, slots.to(u.device)).reshape(-1).contiguous()
+        self._bufs, self._reqs, self._unpack = [], [], []
+        for nb, ix in self.send:
+            buf = u.index_select(0, ix.to(u.device)).contiguous()
             self._bufs.append(buf)
             self._reqs.append(dist.isend(buf, nb, group=self.group))
-        for nb, a, e in self.recv:
-            self._reqs.append(dist.irecv(cells[a:e].reshape(-1), nb, group=self.group))
+        for nb, ix, contiguous in self.recv:
+            if contiguous:
+                a = int(ix[0])
+                self._reqs.append(dist.irecv(u[a:a + len(ix)], nb, group=self.group))
+            else:
+                buf = torch.empty(len(ix), dtype=u.dtype, device=u.device)
+                self._unpack.append((ix, buf))
+                self._reqs.append(dist.irecv(buf, nb, group=self.group))
 
     def finish_update(self, u):
         if self._reqs is None:
             raise RuntimeError("finish_ghost_update: no update was started on this vector")
         for r in self._reqs:
             r.wait()
-        self._reqs, self._bufs = None, None
+        for ix, buf in self._unpack:
+            u.index_copy_(0, ix.to(u.device), buf)
+        self._reqs, self._bufs, self._unpack = None, None, None
 
     # compress (ghost_exchange.cpp:359-398)
     def compress(self, y):
-        cells = self._cells(y)
         reqs, incoming = [], []
-        for nb, a, e in self.recv:
-            reqs.append(dist.isend(cells[a:e].reshape(-1).contiguous(), nb, group=self.group))
-        for nb, slots in self.send:
-            buf = torch.empty(len(slots) * self.nq, dtype=y.dtype, device=y.device)
-            incoming.append((nb, slots, buf))
+        for nb, ix, _ in self.recv:
+            reqs.append(dist.isend(y.index_select(0, ix.to(y.device)).contiguous(), nb,
+                                   group=self.group))
+        for nb, ix in self.send:
+            buf = torch.empty(len(ix), dtype=y.dtype, device=y.device)
+            incoming.append((ix, buf))
             reqs.append(dist.irecv(buf, nb, group=self.group))
         for r in reqs:
             r.wait()
         # ascending source rank: plans are sorted by neighbour
-        for nb, slots, buf in incoming:
-            cells.index_add_(0, slots.to(y.device), buf.view(-1, self.nq))
-        cells[self.n_owned:] = 0
+        for ix, buf in incoming:
+            y.index_add_(0, ix.to(y.device), buf)
+        y[self.owned_size:] = 0
 
 
 def exchange_apply(exchanger, phase1, phase2, u, y):

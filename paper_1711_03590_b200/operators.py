@@ -132,9 +132,13 @@ def assign_face_owners(mesh: Mesh, faces: np.ndarray, partition: Partition):
     partition.face_owner = fo
 
 
+BASIS_KINDS = {"lagrange_gauss_lobatto": 0, "lagrange_gauss": 1, "hermite_like": 2}
+
+
 @dataclass
 class OperatorConfig:
-    """dg::OperatorConfig (operators.hpp:26-51) for this path."""
+    """dg::OperatorConfig (operators.hpp:26-51) for this path. basis: one of
+    BASIS_KINDS (BasisKind, basis.hpp:10-15)."""
     d: int = 3
     p: int = 3
     W: int = 1
@@ -145,6 +149,15 @@ class OperatorConfig:
 
     def k(self):
         return self.p + 1
+
+
+def make_operator_config(kind="laplacian", d=3, p=3, W=1, geometry="g3",
+                         precision="fp64") -> OperatorConfig:
+    """make_operator_config (operators.cpp:27-41): the Laplacian at p >= 3
+    uses the Hermite-like basis, everything else the nodal Gauss-Lobatto one."""
+    basis = "hermite_like" if kind == "laplacian" and p >= 3 else "lagrange_gauss_lobatto"
+    return OperatorConfig(d=d, p=p, W=W, kind=kind, basis=basis, geometry=geometry,
+                          precision=precision)
 
 
 @dataclass
@@ -208,9 +221,8 @@ class RankOperator:
         if config.kind != "laplacian":
             raise _lib.DgxInvalidArgument(
                 "RankOperator: this path implements the Laplacian only")
-        if config.basis != "lagrange_gauss_lobatto":
-            raise _lib.DgxInvalidArgument(
-                "RankOperator: only the nodal Gauss-Lobatto basis is implemented")
+        if config.basis not in BASIS_KINDS:
+            raise _lib.DgxInvalidArgument(f"RankOperator: unknown basis {config.basis!r}")
         self.mesh, self.config, self.rank = mesh, config, rank
         faces = np.ascontiguousarray(faces, FACE_DTYPE)
         if len(partition.face_owner) != len(faces):
@@ -226,7 +238,7 @@ class RankOperator:
         s.cell_owner, s.rank_cell_range, s.face_owner = co.ctypes.data, rr.ctypes.data, fo.ctypes.data
         s.rank = rank
         s.config.d, s.config.p, s.config.W = config.d, config.p, config.W
-        s.config.basis = 0
+        s.config.basis = BASIS_KINDS[config.basis]
         s.config.geometry_variant = 3 if config.geometry == "g3" else -1
         s.config.precision = {"fp64": 0, "fp32": 1}[config.precision]
         g = s.geometry
@@ -324,6 +336,41 @@ class RankOperator:
             check(lib().dgx_get_plan(self._h, C.c_int(w), C.c_int(i), None,
                                      None, None, cells.ctypes.data_as(C.c_void_p)))
             out.append((nb.value, cells))
+        return out
+
+    def plan_dofs(self, which):
+        """NeighborPlan::dof_offsets / dofs per plan (ghost_exchange.hpp:29-52):
+        list of (offsets uint32[n_cells+1], dofs uint32[n_values])."""
+        w = 0 if which == "send" else 1
+        out = []
+        for i in range(len(self.plans(which))):
+            nd = C.c_int64()
+            check(lib().dgx_get_plan_dofs(self._h, C.c_int(w), C.c_int(i), None,
+                                          C.byref(nd), None))
+            nc = C.c_int64()
+            check(lib().dgx_get_plan(self._h, C.c_int(w), C.c_int(i), None, None,
+                                     C.byref(nc), None))
+            offs = np.empty(nc.value + 1, np.uint32)
+            dofs = np.empty(nd.value, np.uint32)
+            check(lib().dgx_get_plan_dofs(self._h, C.c_int(w), C.c_int(i),
+                                          offs.ctypes.data_as(C.c_void_p), None,
+                                          dofs.ctypes.data_as(C.c_void_p)))
+            out.append((offs, dofs))
+        return out
+
+    def plan_values(self, which):
+        """Flat value indices (slot * k^d + dof) of every plan, in plan order --
+        what the transports pack / unpack."""
+        lay = self._layout
+        nq = lay.dofs_per_cell
+        out = []
+        for (nb, cells), (offs, dofs) in zip(self.plans(which), self.plan_dofs(which)):
+            c = cells.astype(np.int64)
+            owned = (c >= lay.owned_cell_begin) & (c < lay.owned_cell_begin + lay.n_owned_cells)
+            slots = np.where(owned, c - lay.owned_cell_begin,
+                             lay.n_owned_cells + np.searchsorted(lay.ghost_global_cells, c))
+            per = np.diff(offs.astype(np.int64))
+            out.append((nb, np.repeat(slots, per) * nq + dofs.astype(np.int64)))
         return out
 
     def device_geometry(self, which):

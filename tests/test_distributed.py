@@ -19,7 +19,8 @@ import torch.multiprocessing as mp
 from conftest import Case, rel_linf
 
 CASES = ["def2d_periodic_p2_r4", "c3_vertex_p4_r3", "def3d_p3_m2_r2", "c4_vertex_coef_p5_r2",
-         "cart3d_ragged_p4_r3"]
+         "cart3d_ragged_p4_r3", "herm3d_p5_m2_r3", "herm_c4_vertex_coef_p5_r2",
+         "gauss3d_p3_m2_r2"]
 
 
 def _free_port():
@@ -43,12 +44,13 @@ def _worker(rank, world, port, name, q):
         faces = dgx.enumerate_faces(mesh)
         part = dgx.partition_cells(mesh, world)
         dgx.assign_face_owners(mesh, faces, part)
-        op = dgx.RankOperator(mesh, part, faces, dgx.Geometry(), dgx.OperatorConfig(d=c.d, p=c.p),
+        op = dgx.RankOperator(mesh, part, faces, dgx.Geometry(),
+                              dgx.OperatorConfig(d=c.d, p=c.p, basis=c.basis_name),
                               rank, device=-1)
         lay = op.layout()
         ex = TorchExchanger.from_operator(op)
         P = O.Problem(c.d, c.cells, c.p, periodic=c.periodic, deform=c.deform(),
-                      coefficient=c.coefficient, n_ranks=world)
+                      coefficient=c.coefficient, n_ranks=world, basis=c.basis)
         nq = lay.dofs_per_cell
         x = c.g[f"x{c.seeds[0]}"]
         b, e = lay.owned_cell_begin, lay.owned_cell_begin + lay.n_owned_cells
@@ -63,8 +65,17 @@ def _worker(rank, world, port, name, q):
         def phase2(uu, yy):
             # oracle stand-in for the device kernel: rank-local apply with the
             # ghost values delivered by the update
-            assert not torch.isnan(uu).any(), "ghost update incomplete"
-            yy.copy_(torch.from_numpy(P.apply_rank_local(rank, uu.numpy())))
+            got = torch.zeros(lay.total_size, dtype=torch.bool)
+            for _, ix in op.plan_values("recv"):
+                got[torch.from_numpy(ix)] = True
+            assert not torch.isnan(uu[got]).any(), "ghost update incomplete"
+            # only the planned dofs travel (whole cells, or two layers per
+            # coupled face for the Hermite-like basis); the rest stays unset
+            # and must not be read
+            assert bool(torch.isnan(uu[lay.owned_size:]).any()) == (c.basis == 2)
+            v = torch.where(got | (torch.arange(lay.total_size) < lay.owned_size), uu,
+                            torch.zeros_like(uu))
+            yy.copy_(torch.from_numpy(P.apply_rank_local(rank, v.numpy())))
 
         exchange_apply(ex, phase1, phase2, u, y)
         assert torch.all(y[lay.owned_size:] == 0)

@@ -53,7 +53,7 @@ def build(c: Case, rank=0, n_ranks=None, precision="fp64", p=None):
     faces = D.enumerate_faces(mesh)
     part = D.partition_cells(mesh, n_ranks or c.n_ranks)
     D.assign_face_owners(mesh, faces, part)
-    cfg = D.OperatorConfig(d=c.d, p=p or c.p, precision=precision)
+    cfg = D.OperatorConfig(d=c.d, p=p or c.p, precision=precision, basis=c.basis_name)
     return D.RankOperator(mesh, part, faces, geometry_of(c), cfg, rank), part
 
 
@@ -66,9 +66,11 @@ def apply_single(torch, op, x, dtype=None):
     return y.double().cpu().numpy()
 
 
-def apply_serial_ranks(torch, ops, parts, x, nq, return_local=False):
+def apply_serial_ranks(torch, ops, parts, x, nq, return_local=False, planned_only=False):
     """SerialRanks (reference tests/test_operators.cpp:446-535): ghost fill by
-    copy, both phases on the device per rank, compress on the host."""
+    copy, both phases on the device per rank, compress on the host.
+    planned_only: only the dofs of the receive plans are filled (what the
+    exchange ships), every other ghost value is NaN and must not be read."""
     y = np.zeros_like(x)
     local = []
     for r, op in enumerate(ops):
@@ -77,6 +79,12 @@ def apply_serial_ranks(torch, ops, parts, x, nq, return_local=False):
         e = b + lay.n_owned_cells
         u_loc = np.concatenate([x[b * nq:e * nq]] +
                                [x[g * nq:(g + 1) * nq] for g in lay.ghost_global_cells])
+        if planned_only:
+            keep = np.zeros(u_loc.size, bool)
+            keep[: lay.owned_size] = True
+            for _, ix in op.plan_values("recv"):
+                keep[ix] = True
+            u_loc = np.where(keep, u_loc, np.nan)
         u = torch.tensor(u_loc, device="cuda")
         yl = torch.full_like(u, float("nan"))
         op.apply_phase(1, u, yl)
@@ -111,13 +119,15 @@ def test_golden_rank_partitioned(torch, name):
         parts.append(part)
     nq = (c.p + 1) ** c.d
     x = c.g[f"x{c.seeds[0]}"]
-    y, local = apply_serial_ranks(torch, ops, parts, x, nq, return_local=True)
+    y, local = apply_serial_ranks(torch, ops, parts, x, nq, return_local=True,
+                                  planned_only=c.basis == 2)
     assert rel_linf(y, c.g[f"y{c.seeds[0]}"]) < TOL64
     # per-rank state before compress (ghost slots hold remote contributions)
     P = O.Problem(c.d, c.cells, c.p, periodic=c.periodic, deform=c.deform(),
-                  coefficient=c.coefficient, n_ranks=c.n_ranks)
+                  coefficient=c.coefficient, n_ranks=c.n_ranks, basis=c.basis)
     for r, (u_loc, y_loc) in enumerate(local):
-        assert rel_linf(y_loc, P.apply_rank_local(r, u_loc)) < TOL64
+        assert np.all(np.isfinite(y_loc))
+        assert rel_linf(y_loc, P.apply_rank_local(r, np.nan_to_num(u_loc, nan=0.0))) < TOL64
 
 
 @pytest.mark.parametrize("name", [n for n in NAMES if n.startswith(("c1", "def3d", "c3", "c4", "c5", "def2d_p3"))])
@@ -177,12 +187,48 @@ RANDOM = [
 ]
 
 
-@pytest.mark.parametrize("cfg", RANDOM, ids=lambda c: f"d{c[0]}p{c[2]}r{c[6]}{'P' if c[3] else 'D'}{c[4][0][0] if c[4] else 'C'}{'a' if c[5] else ''}")
+def _cfg_id(c):
+    return (f"d{c[0]}p{c[2]}r{c[6]}{'P' if c[3] else 'D'}{c[4][0][0] if c[4] else 'C'}"
+            f"{'a' if c[5] else ''}{'' if len(c) < 8 else '-' + c[7]}")
+
+
+@pytest.mark.parametrize("cfg", RANDOM, ids=_cfg_id)
 def test_random_configs_against_oracle(torch, cfg):
+    run_random_config(torch, cfg)
+
+
+# the reference default basis for the Laplacian at p >= 3 (Hermite-like,
+# operators.cpp:27-41) and the Lagrange-Gauss collocation basis; multi-rank
+# cases fill only the planned ghost dofs (two layers per coupled face)
+RANDOM_BASES = [
+    (3, [3, 3, 2], p, bool(p % 2), ("reference", 0.04, 2), False, 1, "hermite_like")
+    for p in range(3, 11)
+] + [
+    (2, [5, 4], p, bool(p % 2), ("reference", 0.05, 2), False, 1, "hermite_like")
+    for p in range(3, 11)
+] + [
+    (3, [4, 3, 3], 5, False, ("vertex", 0.1), True, 3, "hermite_like"),
+    (3, [3, 4, 3], 4, True, None, False, 4, "hermite_like"),
+    (2, [7, 5], 6, False, ("vertex", 0.1), False, 3, "hermite_like"),
+    (3, [3, 3, 3], 8, False, ("reference", 0.05, 2), False, 2, "hermite_like"),
+    (3, [3, 3, 2], 2, False, ("reference", 0.04, 2), False, 2, "lagrange_gauss"),
+    (3, [3, 2, 2], 5, True, None, False, 1, "lagrange_gauss"),
+    (2, [5, 4], 7, False, ("vertex", 0.1), True, 3, "lagrange_gauss"),
+]
+
+
+@pytest.mark.parametrize("cfg", RANDOM_BASES, ids=_cfg_id)
+def test_other_bases_against_oracle(torch, cfg):
+    run_random_config(torch, cfg)
+
+
+def run_random_config(torch, cfg):
     from oracle import oracle as O
     D = dgx()
-    d, cells, p, periodic, deform, coef, nr = cfg
-    P = O.Problem(d, cells, p, periodic=periodic, deform=deform, coefficient=coef, n_ranks=nr)
+    d, cells, p, periodic, deform, coef, nr = cfg[:7]
+    basis = cfg[7] if len(cfg) > 7 else "lagrange_gauss_lobatto"
+    P = O.Problem(d, cells, p, periodic=periodic, deform=deform, coefficient=coef, n_ranks=nr,
+                  basis=O.BASIS[basis])
     amp = deform[1] if deform and deform[0] == "reference" else 0.0
     m = deform[2] if deform and deform[0] == "reference" else 1
     mesh = D.make_box_mesh(d, cells, amp, periodic, m)
@@ -195,11 +241,13 @@ def test_random_configs_against_oracle(torch, cfg):
     for r in range(nr):
         part = D.partition_cells(mesh, nr)
         D.assign_face_owners(mesh, faces, part)
-        ops.append(D.RankOperator(mesh, part, faces, geo, D.OperatorConfig(d=d, p=p), r))
+        ops.append(D.RankOperator(mesh, part, faces, geo, D.OperatorConfig(d=d, p=p, basis=basis),
+                                  r))
     if nr == 1:
         y = apply_single(torch, ops[0], x)
     else:
-        y = apply_serial_ranks(torch, ops, None, x, (p + 1) ** d)
+        y = apply_serial_ranks(torch, ops, None, x, (p + 1) ** d,
+                               planned_only=basis == "hermite_like")
     assert rel_linf(y, y_ref) < TOL64 and rel_l2(y, y_ref) < TOL64, (rel_linf(y, y_ref), rel_l2(y, y_ref))
 
 

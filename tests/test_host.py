@@ -60,7 +60,7 @@ def host_op(c: Case, rank, n_ranks=None, p=None):
     faces = dgx.enumerate_faces(mesh)
     part = dgx.partition_cells(mesh, n_ranks or c.n_ranks)
     dgx.assign_face_owners(mesh, faces, part)
-    cfg = dgx.OperatorConfig(d=c.d, p=p or c.p)
+    cfg = dgx.OperatorConfig(d=c.d, p=p or c.p, basis=c.basis_name)
     return dgx.RankOperator(mesh, part, faces, dgx.Geometry(), cfg, rank, device=-1), faces, part
 
 
@@ -78,8 +78,16 @@ def test_layout_and_plans_bitwise(name):
             plans = op.plans(which)
             nbs = c.g[f"r{r}_{which}_neighbors"]
             assert [nb for nb, _ in plans] == list(nbs)
-            for i, (_, cells) in enumerate(plans):
+            for i, ((_, cells), (offs, dofs)) in enumerate(zip(plans, op.plan_dofs(which))):
                 assert np.array_equal(cells, c.g[f"r{r}_{which}{i}_cells"])
+                key = f"r{r}_{which}{i}_dofs"
+                if key in c.g:  # Hermite-like: two layers per coupled face
+                    assert np.array_equal(offs, c.g[f"r{r}_{which}{i}_offsets"])
+                    assert np.array_equal(dofs, c.g[key])
+                else:  # whole cells travel
+                    nq = lay.dofs_per_cell
+                    assert np.array_equal(offs, np.arange(len(cells) + 1) * nq)
+                    assert np.array_equal(dofs, np.tile(np.arange(nq), len(cells)))
         # receive plans concatenated = ghost storage order: NCCL receives land
         # directly in the ghost region
         recv = [cells for _, cells in op.plans("recv")]
@@ -148,9 +156,12 @@ def test_error_mapping():
         dgx.RankOperator(mesh, part, faces, dgx.Geometry(), dgx.OperatorConfig(d=2, p=0), 0, -1)
     with pytest.raises(dgx.DgxInvalidArgument):
         dgx.RankOperator(mesh, part, faces, dgx.Geometry(), dgx.OperatorConfig(d=2, p=3, W=3), 0, -1)
+    with pytest.raises(dgx.DgxInvalidArgument, match="Hermite"):
+        dgx.RankOperator(mesh, part, faces, dgx.Geometry(),
+                         dgx.OperatorConfig(d=2, p=2, basis="hermite_like"), 0, -1)
     with pytest.raises(dgx.DgxInvalidArgument):
         dgx.RankOperator(mesh, part, faces, dgx.Geometry(),
-                         dgx.OperatorConfig(d=2, p=3, basis="hermite_like"), 0, -1)
+                         dgx.OperatorConfig(d=2, p=3, basis="bernstein"), 0, -1)
     with pytest.raises(dgx.DgxInvalidArgument):
         dgx.RankOperator(mesh, part, faces, dgx.Geometry(), dgx.OperatorConfig(d=3, p=3), 0, -1)
     with pytest.raises(dgx.DgxInvalidArgument):
@@ -162,6 +173,37 @@ def test_error_mapping():
     bad["interior_cell"][0] = 10 ** 6
     with pytest.raises(dgx.DgxInvalidArgument):
         dgx.RankOperator(mesh, part, bad, dgx.Geometry(), dgx.OperatorConfig(d=2, p=3), 0, -1)
+
+
+def R_available():
+    from oracle import reflib as R
+    return R.available()
+
+
+@pytest.mark.skipif(not R_available(), reason="reference library not built")
+@pytest.mark.parametrize("cfg", [(3, [4, 3, 5], 4, 5, False), (2, [7, 6], 6, 4, True),
+                                 (3, [3, 3, 3], 3, 2, True)])
+def test_hermite_plans_match_reference(cfg):
+    """Two-layer exchange plans of the Hermite-like basis against the
+    reference's build_exchange_plan on more partitions than the fixtures."""
+    from oracle import reflib as R
+    d, cells, p, nr, periodic = cfg
+    w = R.World(d, cells, p, n_ranks=nr, periodic=periodic, basis="hermite")
+    mesh = dgx.make_box_mesh(d, cells, 0.0, periodic, 1)
+    faces = dgx.enumerate_faces(mesh)
+    part = dgx.partition_cells(mesh, nr)
+    dgx.assign_face_owners(mesh, faces, part)
+    for r in range(nr):
+        op = dgx.RankOperator(mesh, part, faces, dgx.Geometry(),
+                              dgx.OperatorConfig(d=d, p=p, basis="hermite_like"), r, -1)
+        for which in ("send", "recv"):
+            ref = w.plans(r, which)
+            mine = op.plans(which)
+            assert [nb for nb, _ in mine] == [q["neighbor"] for q in ref]
+            for (nb, cells_), (offs, dofs), q in zip(mine, op.plan_dofs(which), ref):
+                assert np.array_equal(cells_, q["cells"])
+                assert np.array_equal(offs, q["offsets"])
+                assert np.array_equal(dofs, q["dofs"])
 
 
 def test_large_topology_matches_oracle():
