@@ -1,7 +1,7 @@
 """Benchmark of the B200 SIPG-Laplacian apply (BASELINE.json metric).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
-                    [--config c4|c3|c5|c5f32|c1|c2] [--cells n]
+                    [--config c4|c3|c5|c5f32|c1|c2|c4h|c3h|c5h] [--cells n]
 
 One step = one y = A u over the whole mesh (all ranks). Default workload:
 BASELINE.json configs[3] ("C4"): 3D SIPG Laplacian, deformed 128^3-cell hex
@@ -46,11 +46,23 @@ CONFIGS = {
            "C1: 3D SIPG, periodic Cartesian 16^3, p=3, fp64"),
     "c2": (2, 256, 5, False, "cart", False, "fp64", 1,
            "C2: 2D SIPG, Dirichlet Cartesian 256^2, p=5, fp64"),
+    # the same workloads with the reference's default Laplacian basis for
+    # p >= 3, Hermite-like (make_operator_config, operators.cpp:27-41)
+    "c4h": (3, 128, 5, False, "vertex", True, "fp64", 3,
+            "C4h: 3D SIPG, deformed 128^3, p=5, a(x) folded, Hermite-like basis, fp64"),
+    "c3h": (3, 64, 4, False, "vertex", False, "fp64", 2,
+            "C3h: 3D SIPG, deformed 64^3, p=4, Hermite-like basis, fp64"),
+    "c5h": (3, 160, 6, False, "cart", False, "fp64", 4,
+            "C5h: 3D SIPG, Cartesian 160^3, p=6, affine, Hermite-like basis, fp64"),
 }
+# BasisKind per config (default: the nodal Gauss-Lobatto basis BASELINE names)
+BASIS = {"c4h": "hermite_like", "c3h": "hermite_like", "c5h": "hermite_like"}
 # reference instrumented flop count per DoF (counters x W / applies,
 # bench.cpp:339), SURVEY.md s.8d
 REF_FLOPS_PER_DOF = {"c4": 240.0, "c3": 215.52, "c5": 260.82, "c5f32": 260.82,
-                     "c1": 198.0, "c2": 105.80}
+                     "c1": 198.0, "c2": 105.80,
+                     # Hermite-like: plain (not even-odd) S passes, same counters
+                     "c4h": 268.0, "c3h": 242.4, "c5h": 293.14}
 
 
 def peaks():
@@ -160,7 +172,8 @@ class RefBench:
             geo["compressed"] = False
         best = None
         for W in (4, 8):
-            w = R.World(d, cells, p, n_ranks=self.n_ranks, periodic=periodic, W=W, geometry=geo)
+            w = R.World(d, cells, p, n_ranks=self.n_ranks, periodic=periodic, W=W, geometry=geo,
+                        basis=BASIS.get(cfg_name, "lagrange_gauss_lobatto"))
             w.time(1)
             t = min(w.time(1) for _ in range(3))
             if best is None or t < best[0]:
@@ -171,7 +184,8 @@ class RefBench:
         # ceil(0.02 s / est) applies per repetition, bench.cpp:309-319)
         self.inner = max(1, int(np.ceil(0.5 / max(t1, 1e-6))))
         self.sample = (f"{label.split(':')[0]} shape at {sample_cells}^{d} cells "
-                       f"({self.n_dofs} DoFs), reference RankOperator::apply, GL basis, "
+                       f"({self.n_dofs} DoFs), reference RankOperator::apply, "
+                       f"{BASIS.get(cfg_name, 'lagrange_gauss_lobatto')} basis, "
                        f"W={self.W}, R={self.n_ranks} threaded ranks (run_ranks + "
                        f"GhostExchanger), {self.inner} applies per step")
 
@@ -204,6 +218,7 @@ def main():
     n_dofs = n ** d * (p + 1) ** d
     metric = "DG Laplacian apply throughput (DoFs/s)"
     config = {"workload": label, "cells": [n] * d, "degree": p, "n_dofs": n_dofs,
+              "basis": BASIS.get(args.config, "lagrange_gauss_lobatto"),
               "seed": seed, "partition": f"contiguous lexicographic slabs x{args.gpus}",
               "l2": "inputs larger than L2 (no flush)"}
 
@@ -243,7 +258,8 @@ def main():
     dgx.assign_face_owners(mesh, faces, part)
     geo = (dgx.Geometry(source="vertex_bump", vertex_bump_eps=0.1, coefficient="a1" if coef else None)
            if kind == "vertex" else dgx.Geometry(source="mesh"))
-    op = dgx.RankOperator(mesh, part, faces, geo, dgx.OperatorConfig(d=d, p=p, precision=prec),
+    op = dgx.RankOperator(mesh, part, faces, geo, dgx.OperatorConfig(d=d, p=p, precision=prec,
+                                         basis=BASIS.get(args.config, "lagrange_gauss_lobatto")),
                           rank, device=local)
     lay = op.layout()
     hooks = None
