@@ -168,6 +168,23 @@ dgx_status dgx_get_plan(const dgx_op *op, int which, int idx, int *n_plans,
 dgx_status dgx_get_plan_dofs(const dgx_op *op, int which, int idx, uint32_t *dof_offsets,
                              int64_t *n_dofs, uint32_t *dofs);
 
+/* Physical quadrature points of the operator's mapping (the reference
+ * evaluates forcing and Dirichlet data there, operators.cpp:545-560,
+ * 1115-1145; unavailable for DGX_GEOMETRY_HOST_ARRAYS): which 0: owned cells
+ * [cell][q][d] (q lexicographic, axis 0 fastest); 1: the faces this rank
+ * computes [face][qf][d] (GeometryCache::face_qpoints order, dgx_get_geometry
+ * which=3 gives their global ids); 2: boundary flag (0/1) per computed face.
+ * Pass out=NULL to query n. */
+dgx_status dgx_get_quadrature_points(dgx_op *op, int which, double *out, int64_t *n);
+/* RankOperator::assemble_rhs (operators.cpp:266-282): rhs = forcing
+ * (f det(J) w_q tested with the basis, :1115-1145) + the Dirichlet data moved
+ * to the right-hand side by the boundary faces (:1033-1111). f: device
+ * [owned cell][q] values f(x_q), g: device [computed face][qf] values g(x_qf)
+ * (only boundary faces are read); either may be NULL (zero). rhs: device,
+ * layout total_size, overwritten; the ghost region is zero. fp64 only. */
+dgx_status dgx_assemble_rhs(dgx_op *op, const double *f, const double *g, double *rhs,
+                            void *stream);
+
 /* Replaces dg::ExchangeHooks (operators.hpp:61-66). Each hook receives the
  * device vector and the stream of the apply; it must leave its work ordered
  * on that stream. */

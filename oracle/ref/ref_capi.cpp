@@ -25,7 +25,9 @@
 #include <dg/quadrature.hpp>
 #include <dg/solvers.hpp>
 
+#include <array>
 #include <chrono>
+#include <cmath>
 #include <cstdint>
 #include <cstring>
 #include <memory>
@@ -39,6 +41,23 @@ namespace
 {
 thread_local std::string g_err;
 thread_local int g_basis = 0; // BasisKind for new worlds; -1 = reference default
+thread_local int g_manufactured = 0; // forcing/dirichlet of the convergence study
+
+// The manufactured solution of the reference convergence study
+// (bench.cpp:437-459), restated here as test input.
+double mf_solution(int d, const std::array<double, 3> &x)
+{
+  double u = std::cos(2.3 * x[0] + 0.4);
+  u *= std::cos(1.7 * x[1] - 0.2);
+  if (d == 3)
+    u *= std::cos(1.1 * x[2] + 0.1);
+  return u;
+}
+double mf_neg_laplacian(int d, const std::array<double, 3> &x)
+{
+  const double lam = 2.3 * 2.3 + 1.7 * 1.7 + (d == 3 ? 1.1 * 1.1 : 0.0);
+  return lam * mf_solution(d, x);
+}
 
 template <typename F>
 int guard(F &&f)
@@ -110,6 +129,11 @@ World *make_world_common(int d, const int *cells, double amplitude,
                                 GeometryVariant::g3);
   if (g_basis >= 0)
     w->cfg.basis = static_cast<BasisKind>(g_basis); // GL unless selected
+  if (g_manufactured)
+    {
+      w->cfg.dirichlet = [d](const std::array<double, 3> &x) { return mf_solution(d, x); };
+      w->cfg.forcing = [d](const std::array<double, 3> &x) { return mf_neg_laplacian(d, x); };
+    }
   w->faces = enumerate_faces(w->mesh);
   w->partition = partition_cells(w->mesh, n_ranks);
   assign_face_owners(w->mesh, w->faces, w->partition);
@@ -153,6 +177,13 @@ int dgref_set_basis(int kind)
       throw std::invalid_argument("dgref_set_basis: unknown basis kind");
     g_basis = kind;
   });
+}
+
+// Worlds created next carry the manufactured forcing / Dirichlet data of the
+// convergence study (bench.cpp:525-560) when flag != 0.
+int dgref_set_manufactured(int flag)
+{
+  return guard([&] { g_manufactured = flag; });
 }
 
 // Shape matrices of the selected basis (dgref_set_basis; -1 resolves as for
@@ -450,6 +481,19 @@ int dgref_world_apply_rank_local(void *wp, int rank, const double *u_local,
     u.state = VectorState::ghosts_valid;
     w.ops[rank]->apply(u, y, &hooks);
     std::memcpy(y_local, y.data.data(), sizeof(double) * l.total_size);
+  });
+}
+
+// RankOperator::assemble_rhs of one rank (operators.cpp:266-282), rank-local
+// layout (W = 1 worlds: owned cells then ghosts).
+int dgref_world_rhs(void *wp, int rank, double *rhs_local)
+{
+  return guard([&] {
+    World &w = *static_cast<World *>(wp);
+    const DoFLayout &l = w.ops.at(rank)->layout();
+    GhostedVector r = l.make_vector();
+    w.ops[rank]->assemble_rhs(r);
+    std::memcpy(rhs_local, r.data.data(), sizeof(double) * l.total_size);
   });
 }
 

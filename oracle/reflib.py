@@ -46,6 +46,21 @@ def _p(a):
     return a.ctypes.data_as(C.c_void_p) if a is not None else None
 
 
+def manufactured_solution(d, x):
+    """exact_solution of the reference convergence study (bench.cpp:437-444);
+    x: [..., d] physical points."""
+    u = np.cos(2.3 * x[..., 0] + 0.4) * np.cos(1.7 * x[..., 1] - 0.2)
+    if d == 3:
+        u = u * np.cos(1.1 * x[..., 2] + 0.1)
+    return u
+
+
+def manufactured_forcing(d, x):
+    """exact_neg_laplacian (bench.cpp:455-459)."""
+    lam = 2.3 * 2.3 + 1.7 * 1.7 + (1.1 * 1.1 if d == 3 else 0.0)
+    return lam * manufactured_solution(d, x)
+
+
 def random_vector(n: int, seed: int) -> np.ndarray:
     """std::mt19937(seed) + uniform_real_distribution<double>(-1,1)."""
     out = np.empty(n, np.float64)
@@ -101,10 +116,17 @@ class World:
     rank (proj/tests/test_ghost_exchange.cpp:20-50)."""
 
     def __init__(self, d, cells, p, n_ranks=1, amplitude=0.0,
-                 mapping_degree=1, periodic=False, W=1, geometry=None, basis="gl"):
-        with _basis(basis):
-            self._create(d, cells, p, n_ranks, amplitude, mapping_degree, periodic, W,
-                         geometry)
+                 mapping_degree=1, periodic=False, W=1, geometry=None, basis="gl",
+                 manufactured=False):
+        """manufactured: forcing / Dirichlet data of the reference convergence
+        study (bench.cpp:437-560) for rhs()."""
+        _chk(lib().dgref_set_manufactured(C.c_int(int(manufactured))))
+        try:
+            with _basis(basis):
+                self._create(d, cells, p, n_ranks, amplitude, mapping_degree, periodic, W,
+                             geometry)
+        finally:
+            lib().dgref_set_manufactured(C.c_int(0))
 
     def _create(self, d, cells, p, n_ranks, amplitude, mapping_degree, periodic, W,
                 geometry):
@@ -220,6 +242,13 @@ class World:
         a = np.empty((n, n))
         _chk(lib().dgref_world_assemble(self._h, _p(a)))
         return a
+
+    def rhs(self, rank=0):
+        """RankOperator::assemble_rhs of one rank, rank-local layout (W=1)."""
+        n = self.layout(rank)["total_size"]
+        out = np.empty(n)
+        _chk(lib().dgref_world_rhs(self._h, C.c_int(rank), _p(out)))
+        return out
 
     def cg(self, b, rel_tol=1e-10, max_iterations=10000):
         """conjugate_gradient(make_apply(op), b, x) of the reference."""

@@ -110,7 +110,8 @@ EXPORTS = [
     "dgx_last_error", "dgx_version", "dgx_enumerate_faces", "dgx_partition",
     "dgx_create", "dgx_destroy", "dgx_get_layout", "dgx_get_ghost_cells",
     "dgx_get_plan", "dgx_get_plan_dofs", "dgx_apply", "dgx_apply_f32", "dgx_apply_host",
-    "dgx_apply_phase", "dgx_accumulate_plan", "dgx_conjugate_gradient", "dgx_nccl_unique_id",
+    "dgx_apply_phase", "dgx_accumulate_plan", "dgx_conjugate_gradient",
+    "dgx_get_quadrature_points", "dgx_assemble_rhs", "dgx_nccl_unique_id",
     "dgx_exchanger_create", "dgx_exchanger_hooks", "dgx_exchanger_destroy",
     "dgx_get_geometry", "dgx_get_tasks", "dgx_get_stats", "dgx_random_uniform",
 ]

@@ -257,6 +257,25 @@ dgx_status dgx_accumulate_plan(dgx_op *op, int idx, const double *contrib, doubl
   });
 }
 
+dgx_status dgx_get_quadrature_points(dgx_op *op, int which, double *out, int64_t *n)
+{
+  return guard([&] {
+    const std::vector<double> v = op_of(op).quadrature_points(which);
+    if (n)
+      *n = (int64_t)v.size();
+    if (out)
+      std::memcpy(out, v.data(), 8 * v.size());
+  });
+}
+
+dgx_status dgx_assemble_rhs(dgx_op *op, const double *f, const double *g, double *rhs,
+                            void *stream)
+{
+  return guard([&] {
+    op_of(op).assemble_rhs(f, g, rhs, static_cast<cudaStream_t>(stream));
+  });
+}
+
 dgx_status dgx_conjugate_gradient(dgx_op *op, const double *b, double *x, double rel_tol,
                                   int max_iterations, dgx_solve_report *report, void *stream)
 {

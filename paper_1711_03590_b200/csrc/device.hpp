@@ -86,6 +86,8 @@ namespace dev
 {
 template <typename Real>
 struct ApplyParams;
+template <typename Real>
+struct RhsParams;
 }
 
 // sipg.cu (kernels in sipg_gl.cu / sipg_gauss.cu / sipg_hermite.cu);
@@ -95,6 +97,8 @@ int kernel_cells_per_cta(int D, int K);
 template <typename Real>
 void launch_apply(int D, int K, int basis, bool compressed, const dev::ApplyParams<Real> &prm,
                   cudaStream_t s);
+void launch_rhs(int D, int K, int basis, bool compressed, const dev::RhsParams<double> &prm,
+                cudaStream_t s);
 
 // geometry.cu -- device precompute of the g3 arrays from mapping support
 // points (reference geometry.cpp:36-150,248-522), written straight into the
@@ -116,6 +120,11 @@ struct GeometryJob
   double *volume = nullptr;    // scratch [n_slots]
 };
 void run_geometry(const GeometryJob &job, cudaStream_t s);
+// physical quadrature points of the owned cells ([cell][q][d]) with the
+// plain det(J) w_q ([cell][q]), and of the computed faces ([face][qf][d]);
+// any output may be null
+void run_qpoints(const GeometryJob &job, double *cell_x, double *cell_detw, double *face_x,
+                 cudaStream_t s);
 
 // exchange.cu -- halo pack / unpack / compress kernels over the flat value
 // index lists of the exchange plans (slot * k^d + cell-local dof, in plan

@@ -333,22 +333,114 @@ __global__ void face_geometry_kernel(GeometryJob job, GeoConst gc, int *bad)
   job.penalty[f] = tau;
 }
 
-} // namespace
-
-void run_geometry(const GeometryJob &job, cudaStream_t s)
+// Physical quadrature points of the owned cells, x[c][q][d], and the plain
+// det(J) w_q (no coefficient) the forcing integral uses
+// (add_forcing, operators.cpp:1115-1145).
+__global__ void cell_qpoint_kernel(GeometryJob job, GeoConst gc, double *x_out, double *detw)
 {
-  if (job.k > 16 || job.m + 1 > 16 || job.m < 1)
+  const int d = job.d, k = job.k, n = job.m + 1;
+  int nq = 1, pp = 1;
+  for (int a = 0; a < d; ++a)
+    {
+      nq *= k;
+      pp *= n;
+    }
+  const long long gid = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (gid >= (long long)job.n_geo_cells * nq)
+    return;
+  const int c = (int)(gid / nq);
+  const int q = (int)(gid - (long long)c * nq);
+  double xi[3] = {0, 0, 0};
+  int idx = q;
+  for (int a = 0; a < d; ++a)
+    {
+      xi[a] = gc.qp[idx % k];
+      idx /= k;
+    }
+  double x[3], jac[9], jit[9];
+  map_point_jac(gc, d, n, job.support + (long long)c * pp * d, xi, x, jac);
+  const double det = invert_jac(d, jac, jit);
+  if (x_out)
+    for (int a = 0; a < d; ++a)
+      x_out[gid * d + a] = x[a];
+  if (detw)
+    detw[gid] = det * cell_weight(gc, d, k, q);
+}
+
+// Face quadrature points (GeometryCache::face_qpoints, geometry.cpp:415-453):
+// mapped from the interior side, x[f][qf][d].
+__global__ void face_qpoint_kernel(GeometryJob job, GeoConst gc, double *x_out)
+{
+  const int d = job.d, k = job.k, n = job.m + 1;
+  int nqf = 1, pp = 1;
+  for (int a = 0; a < d - 1; ++a)
+    nqf *= k;
+  for (int a = 0; a < d; ++a)
+    pp *= n;
+  const long long gid = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (gid >= job.n_faces * nqf)
+    return;
+  const long long f = gid / nqf;
+  const int q = (int)(gid - f * nqf);
+  const int4 fc = job.faces[f];
+  const int axis = fc.z / 2;
+  double xi[3] = {0, 0, 0};
+  int idx = q;
+  for (int a = 0, t = 0; a < d; ++a)
+    {
+      if (a == axis)
+        continue;
+      xi[a] = gc.qp[idx % k];
+      idx /= k;
+      ++t;
+    }
+  xi[axis] = fc.z % 2 ? 1.0 : 0.0;
+  double xq[3], jac[9];
+  map_point_jac(gc, d, n, job.support + (long long)fc.x * pp * d, xi, xq, jac);
+  for (int a = 0; a < d; ++a)
+    x_out[gid * d + a] = xq[a];
+}
+
+GeoConst make_geo_const(int k, int m)
+{
+  if (k > 16 || m + 1 > 16 || m < 1)
     fail(Code::invalid_argument, "geometry: k or mapping degree out of range");
   GeoConst gc{};
-  const Quad1D g = gauss(job.k);
-  for (int i = 0; i < job.k; ++i)
+  const Quad1D g = gauss(k);
+  for (int i = 0; i < k; ++i)
     {
       gc.qp[i] = g.points[i];
       gc.qw[i] = g.weights[i];
     }
-  const Quad1D gl = gauss_lobatto(job.m + 1);
-  for (int i = 0; i <= job.m; ++i)
+  const Quad1D gl = gauss_lobatto(m + 1);
+  for (int i = 0; i <= m; ++i)
     gc.nodes[i] = gl.points[i];
+  return gc;
+}
+
+} // namespace
+
+void run_qpoints(const GeometryJob &job, double *cell_x, double *cell_detw, double *face_x,
+                 cudaStream_t s)
+{
+  const GeoConst gc = make_geo_const(job.k, job.m);
+  long long nq = 1;
+  for (int a = 0; a < job.d; ++a)
+    nq *= job.k;
+  const int bs = 128;
+  const long long nc = (long long)job.n_geo_cells * nq;
+  if ((cell_x || cell_detw) && nc > 0)
+    cell_qpoint_kernel<<<(unsigned)((nc + bs - 1) / bs), bs, 0, s>>>(job, gc, cell_x, cell_detw);
+  const long long nf = job.n_faces * (nq / job.k);
+  if (face_x && nf > 0)
+    face_qpoint_kernel<<<(unsigned)((nf + bs - 1) / bs), bs, 0, s>>>(job, gc, face_x);
+  cuda_check(cudaGetLastError(), "quadrature point kernels");
+  cuda_check(cudaStreamSynchronize(s), "quadrature point sync");
+}
+
+void run_geometry(const GeometryJob &job, cudaStream_t s)
+{
+  const GeoConst gc = make_geo_const(job.k, job.m);
   DeviceArray<int> bad(1);
   cuda_check(cudaMemsetAsync(bad.get(), 0, sizeof(int), s), "memset");
   long long nq = 1;

@@ -265,6 +265,9 @@ void Operator::build_tasks(const std::vector<RawFace> &faces, const Partition &p
 
 void Operator::build_geometry(const dgx_setup &s, const std::vector<RawFace> &faces)
 {
+  face_boundary_.resize(layout_.my_faces.size());
+  for (std::size_t i = 0; i < layout_.my_faces.size(); ++i)
+    face_boundary_[i] = faces[layout_.my_faces[i]].at_boundary() ? 1 : 0;
   const dgx_geometry &g = s.geometry;
   const long long n_owned = layout_.n_owned;
   const long long n_slots = n_owned + (long long)layout_.ghosts.size();
@@ -399,8 +402,10 @@ void Operator::build_geometry(const dgx_setup &s, const std::vector<RawFace> &fa
       if (g.coefficient != 0 && g.coefficient != 1)
         fail(Code::invalid_argument, "geometry: unknown coefficient");
       compressed_ = cartesian && !g.coefficient;
-      DeviceArray<double> dsup;
+      DeviceArray<double> &dsup = support_;
       dsup.upload(support);
+      has_mapping_ = true;
+      map_degree_ = m;
       std::vector<int4> fl(nmy);
       for (long long i = 0; i < nmy; ++i)
         {
@@ -409,7 +414,7 @@ void Operator::build_geometry(const dgx_setup &s, const std::vector<RawFace> &fa
                             rf.at_boundary() ? -1 : static_cast<int>(layout_.slot(rf.exterior_cell)),
                             rf.interior_face_number, rf.exterior_face_number);
         }
-      DeviceArray<int4> dfl;
+      DeviceArray<int4> &dfl = face_list_;
       dfl.upload(fl);
       DeviceArray<double> vol(n_slots);
       cell_geo_.resize((size_t)n_owned * ncomp * (compressed_ ? 1 : nq_));
@@ -538,6 +543,101 @@ void Operator::accumulate_plan(int idx, const double *contrib, double *y, cudaSt
     fail(Code::invalid_argument, "accumulate_plan: plan index out of range");
   const long long b = send_offsets_[idx], e = send_offsets_[idx + 1];
   launch_scatter_add_values(y, send_index_.get() + b, e - b, contrib, s);
+}
+
+GeometryJob Operator::mapping_job() const
+{
+  if (!has_mapping_)
+    fail(Code::invalid_argument,
+         "quadrature points: the geometry came as host arrays, there is no mapping");
+  GeometryJob job;
+  job.d = d_;
+  job.k = k_;
+  job.m = map_degree_;
+  job.support = support_.get();
+  job.n_geo_cells = static_cast<int>(layout_.n_owned);
+  job.n_faces = (long long)layout_.my_faces.size();
+  job.faces = face_list_.get();
+  return job;
+}
+
+std::vector<double> Operator::quadrature_points(int which)
+{
+  if (host_only_)
+    fail(Code::invalid_argument, "quadrature points: operator was created host-only");
+  cuda_check(cudaSetDevice(device_), "cudaSetDevice");
+  if (which == 2)
+    return std::vector<double>(face_boundary_.begin(), face_boundary_.end());
+  if (which != 0 && which != 1)
+    fail(Code::invalid_argument, "quadrature points: unknown set");
+  const GeometryJob job = mapping_job();
+  DeviceArray<double> x(which == 0 ? (size_t)layout_.n_owned * nq_ * d_
+                                   : layout_.my_faces.size() * (size_t)nqf_ * d_);
+  run_qpoints(job, which == 0 ? x.get() : nullptr, nullptr, which == 1 ? x.get() : nullptr,
+              nullptr);
+  return x.download();
+}
+
+void Operator::ensure_detw()
+{
+  if (cell_detw_.size() == (size_t)layout_.n_owned * nq_)
+    return;
+  cell_detw_.resize((size_t)layout_.n_owned * nq_);
+  if (has_mapping_)
+    {
+      run_qpoints(mapping_job(), nullptr, cell_detw_.get(), nullptr, nullptr);
+      return;
+    }
+  // host-array geometry (the reference's GeometryCache, no coefficient):
+  // JxW is det(J) w_q, or det(J) for a compressed record
+  const std::vector<double> cg = cell_geo_.download();
+  const int ncomp = d_ * d_ + 1;
+  const Quad1D qg = gauss(k_);
+  std::vector<double> dw((size_t)layout_.n_owned * nq_);
+  for (long long c = 0; c < (long long)layout_.n_owned; ++c)
+    for (long long q = 0; q < nq_; ++q)
+      {
+        if (!compressed_)
+          dw[c * nq_ + q] = cg[(c * ncomp + d_ * d_) * nq_ + q];
+        else
+          {
+            double w = 1.0;
+            long long idx = q;
+            for (int a = 0; a < d_; ++a)
+              {
+                w *= qg.weights[idx % k_];
+                idx /= k_;
+              }
+            dw[c * nq_ + q] = cg[c * ncomp + d_ * d_] * w;
+          }
+      }
+  cell_detw_.upload(dw);
+}
+
+void Operator::assemble_rhs(const double *f, const double *g, double *rhs, cudaStream_t s)
+{
+  if (host_only_)
+    fail(Code::invalid_argument, "assemble_rhs: operator was created host-only");
+  if (precision_ != 0)
+    fail(Code::invalid_argument, "assemble_rhs: fp64 operators only");
+  if (!rhs)
+    fail(Code::invalid_argument, "assemble_rhs: null right-hand side");
+  cuda_check(cudaSetDevice(device_), "cudaSetDevice");
+  if (f)
+    ensure_detw();
+  // std::fill(rhs, 0) (operators.cpp:270-272): the ghost region stays zero
+  cuda_check(cudaMemsetAsync(rhs, 0, sizeof(double) * layout_.total_size(), s), "memset");
+  dev::RhsParams<double> prm;
+  prm.f = f;
+  prm.detw = cell_detw_.get();
+  prm.g = g;
+  prm.y = rhs;
+  prm.face_geo = face_geo_.get();
+  prm.penalty = penalty_.get();
+  prm.task_slot = task_slot_.get();
+  prm.task_face = task_face_.get();
+  prm.n_tasks = static_cast<int>(layout_.n_owned); // owned tasks come first
+  launch_rhs(d_, k_, basis_, compressed_, prm, s);
 }
 
 std::vector<double> Operator::geometry(int which) const

@@ -40,6 +40,12 @@ public:
   int n_inner() const { return n_inner_; }
 
   std::vector<double> geometry(int which) const;
+  // physical quadrature points: 0 owned cells [cell][q][d], 1 computed faces
+  // [face][qf][d], 2 boundary flag per computed face (needs a mapping)
+  std::vector<double> quadrature_points(int which);
+  // RankOperator::assemble_rhs (operators.cpp:266-282); f: [owned cell][q],
+  // g: [computed face][qf] device arrays (null: zero)
+  void assemble_rhs(const double *f, const double *g, double *rhs, cudaStream_t s);
   dgx_stats stats() const;
 
   // exchange plans flattened for the transports: value indices into the
@@ -72,6 +78,17 @@ private:
   DeviceArray<int> task_slot_, task_geo_;
   DeviceArray<int2> task_face_;
   int n_inner_ = 0, n_coupled_ = 0;
+
+  // mapping kept for quadrature points / right-hand side (not for
+  // HOST_ARRAYS geometry)
+  bool has_mapping_ = false;
+  int map_degree_ = 1;
+  DeviceArray<double> support_;
+  DeviceArray<int4> face_list_;
+  DeviceArray<double> cell_detw_; // det(J) w_q per owned cell point, lazily
+  std::vector<char> face_boundary_;
+  void ensure_detw();
+  GeometryJob mapping_job() const;
 
   DeviceArray<long long> send_index_, recv_index_;
   std::vector<long long> send_offsets_, recv_offsets_; // in values, size plans+1

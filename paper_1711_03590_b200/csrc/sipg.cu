@@ -9,6 +9,8 @@ namespace dgx
 
 #define DGX_DECL(B)                                                                       \
   void upload_tables_##B(int K);                                                         \
+  void launch_rhs_##B(int D, int K, bool compressed, const dev::RhsParams<double> &prm,   \
+                      cudaStream_t s);                                                   \
   template <typename Real>                                                               \
   void launch_apply_##B(int D, int K, bool compressed, const dev::ApplyParams<Real> &prm, \
                         cudaStream_t s);
@@ -50,6 +52,18 @@ void launch_apply(int D, int K, int basis, bool compressed, const dev::ApplyPara
     case 0: launch_apply_gl<Real>(D, K, compressed, prm, s); break;
     case 1: launch_apply_gauss<Real>(D, K, compressed, prm, s); break;
     case 2: launch_apply_hermite<Real>(D, K, compressed, prm, s); break;
+    default: fail(Code::invalid_argument, "unknown basis kind");
+    }
+}
+
+void launch_rhs(int D, int K, int basis, bool compressed, const dev::RhsParams<double> &prm,
+                cudaStream_t s)
+{
+  switch (basis)
+    {
+    case 0: launch_rhs_gl(D, K, compressed, prm, s); break;
+    case 1: launch_rhs_gauss(D, K, compressed, prm, s); break;
+    case 2: launch_rhs_hermite(D, K, compressed, prm, s); break;
     default: fail(Code::invalid_argument, "unknown basis kind");
     }
 }

@@ -6,6 +6,27 @@ namespace dgx
 namespace dev
 {
 
+// Global load of two consecutive dofs (m, m+1) of the pencil along axis A
+// through face point p. Along axis 0 they are adjacent in memory (the
+// pencil is K contiguous values at K p), and for even K and fp64 16-byte
+// aligned: one vector load instead of two strided scalar ones (halves the
+// L1 sectors of the x-neighbour reads).
+template <typename Real, int D, int K, int A>
+__device__ __forceinline__ void ldg_pair(const Real *un, int p, int m, Real &a, Real &b)
+{
+  if constexpr (A == 0 && sizeof(Real) == 8 && K % 2 == 0)
+    {
+      const double2 v = __ldg(reinterpret_cast<const double2 *>(un + gidx<D, K, A>(p, m)));
+      a = v.x;
+      b = v.y;
+    }
+  else
+    {
+      a = __ldg(un + gidx<D, K, A>(p, m));
+      b = __ldg(un + gidx<D, K, A>(p, m + 1));
+    }
+}
+
 // Both faces of axis A of every cell in the CTA (runs before the
 // quadrature-point phase, so G still holds the reference gradient):
 //  own traces      value and reference gradient at the face points from the
@@ -38,8 +59,10 @@ __device__ __forceinline__ void face_axis_v4(const ApplyParams<Real> &prm, Real 
   int2 tf[2] = {make_int2(-2, 0), make_int2(-2, 0)};
   if (active)
     {
-      tf[0] = prm.task_face[task * 2 * D + 2 * A];
-      tf[1] = prm.task_face[task * 2 * D + 2 * A + 1];
+      // stashed by the prologue (ordered by the forward-pass barriers)
+      const int2 *tfs = reinterpret_cast<const int2 *>(cell + L::OFF_TF);
+      tf[0] = tfs[2 * A];
+      tf[1] = tfs[2 * A + 1];
     }
   // face geometry at face point p (issued first: longest latency)
   Real jxw[2], tau[2], jo[2][D], jb[2][D];
@@ -81,45 +104,62 @@ __device__ __forceinline__ void face_axis_v4(const ApplyParams<Real> &prm, Real 
         }
     }
   // neighbour pencils -> nodal value / normal-derivative layer (own low face
-  // meets the neighbour's high face, row index 1, and vice versa)
-#pragma unroll
-  for (int s = 0; s < 2; ++s)
+  // meets the neighbour's high face, row index 1, and vice versa). Both
+  // neighbours' loads are issued before either is used: one memory latency
+  // per axis, not two.
+  if constexpr (HERM)
     {
-      Real nu = Real(0), nw = Real(0);
-      if (tf[s].x >= 0)
-        {
-          const Real *un = prm.u + (long long)tf[s].x * NQ;
-          if constexpr (HERM)
-            {
-              // two layers: value and derivative live on the edge layer
-              // and its inner neighbour (read_face_dofs, dof_layout.hpp:291-336)
-              const int me = s == 0 ? K - 1 : 0, mi = s == 0 ? K - 2 : 1;
-              const int ro = s == 0 ? K : 0;
-              const Real xe = __ldg(un + gidx<D, K, A>(p, me)) * (sp * hsign<Real, K>(me));
-              const Real xi = __ldg(un + gidx<D, K, A>(p, mi)) * (sp * hsign<Real, K>(mi));
-              nu = tab<Real, K>(T::oSf + ro + me) * xe + tab<Real, K>(T::oSf + ro + mi) * xi;
-              nw = tab<Real, K>(T::oDf + ro + me) * xe + tab<Real, K>(T::oDf + ro + mi) * xi;
-            }
-          else
-            {
-              Real x[K];
+      // two layers: value and derivative live on the edge layer and its
+      // inner neighbour (read_face_dofs, dof_layout.hpp:291-336)
+      Real xe[2], xi[2];
 #pragma unroll
-              for (int m = 0; m < K; ++m)
-                x[m] = __ldg(un + gidx<D, K, A>(p, m));
+      for (int s = 0; s < 2; ++s)
+        {
+          const int me = s == 0 ? K - 1 : 0, mi = s == 0 ? K - 2 : 1;
+          xe[s] = xi[s] = Real(0);
+          if (tf[s].x >= 0)
+            {
+              const Real *un = prm.u + (long long)tf[s].x * NQ;
               if (s == 0)
-                {
-                  nu = dot_row<Real, K, T::oSf + K>(x);
-                  nw = dot_row<Real, K, T::oDf + K>(x);
-                }
+                ldg_pair<Real, D, K, A>(un, p, K - 2, xi[s], xe[s]);
               else
-                {
-                  nu = dot_row<Real, K, T::oSf>(x);
-                  nw = dot_row<Real, K, T::oDf>(x);
-                }
+                ldg_pair<Real, D, K, A>(un, p, 0, xe[s], xi[s]);
             }
         }
-      NB[(2 * s) * FP + fp] = nu;
-      NB[(2 * s + 1) * FP + fp] = nw;
+#pragma unroll
+      for (int s = 0; s < 2; ++s)
+        {
+          const int me = s == 0 ? K - 1 : 0, mi = s == 0 ? K - 2 : 1;
+          const int ro = s == 0 ? K : 0;
+          const Real ve = xe[s] * (sp * hsign<Real, K>(me));
+          const Real vi = xi[s] * (sp * hsign<Real, K>(mi));
+          NB[(2 * s) * FP + fp] =
+            tab<Real, K>(T::oSf + ro + me) * ve + tab<Real, K>(T::oSf + ro + mi) * vi;
+          NB[(2 * s + 1) * FP + fp] =
+            tab<Real, K>(T::oDf + ro + me) * ve + tab<Real, K>(T::oDf + ro + mi) * vi;
+        }
+    }
+  else
+    {
+      Real x[2][K];
+#pragma unroll
+      for (int s = 0; s < 2; ++s)
+        {
+          const Real *un = prm.u + (long long)(tf[s].x >= 0 ? tf[s].x : 0) * NQ;
+#pragma unroll
+          for (int m = 0; m + 1 < K; m += 2)
+            {
+              ldg_pair<Real, D, K, A>(un, p, m, x[s][m], x[s][m + 1]);
+              if (tf[s].x < 0)
+                x[s][m] = x[s][m + 1] = Real(0);
+            }
+          if constexpr (K % 2 == 1)
+            x[s][K - 1] = tf[s].x >= 0 ? __ldg(un + gidx<D, K, A>(p, K - 1)) : Real(0);
+        }
+      NB[fp] = dot_row<Real, K, T::oSf + K>(x[0]);
+      NB[FP + fp] = dot_row<Real, K, T::oDf + K>(x[0]);
+      NB[2 * FP + fp] = dot_row<Real, K, T::oSf>(x[1]);
+      NB[3 * FP + fp] = dot_row<Real, K, T::oDf>(x[1]);
     }
   // own traces from the collocation fields along the normal
   Real own_u[2], own_g[2][D];

@@ -254,7 +254,10 @@ struct SL
   static constexpr int OFF_OUT = (D + 1) * FS;        // 2D faces x (w, rgn)
   static constexpr int OFF_NB = OFF_OUT + 4 * D * FP; // nu_lo, nw_lo, nu_hi, nw_hi
   static constexpr int OFF_DT = OFF_NB + 4 * FP;      // 2(D-1) derivative fields
-  static constexpr int SM_CELL = OFF_DT + 2 * (D - 1) * FP;
+  // 2D int2 face entries (16 D bytes, fp32 or fp64); even offset so that
+  // they stay 8-byte aligned in fp32 too
+  static constexpr int OFF_TF = (OFF_DT + 2 * (D - 1) * FP + 1) / 2 * 2;
+  static constexpr int SM_CELL = OFF_TF + 4 * D;
 };
 
 // index of the m-th entry along axis A of pencil p (remaining axes
@@ -455,6 +458,10 @@ __global__ void __launch_bounds__(KernelShape<D, K>::THREADS, KernelShape<D, K>:
           for (int off = p * LINE; off < bytes; off += P * LINE)
             asm volatile("prefetch.global.L2 [%0];" ::"l"(gp + off));
         }
+      // the task's face entries, read again by every face axis: kept in
+      // shared memory (one L2 round trip less per axis)
+      for (int i = p; i < 2 * D; i += P) // P may be smaller than 2D (2D, K=2)
+        reinterpret_cast<int2 *>(cell + L::OFF_TF)[i] = prm.task_face[task * 2 * D + i];
 #pragma unroll
       for (int phi = 0; phi < 2 * D; ++phi)
         {

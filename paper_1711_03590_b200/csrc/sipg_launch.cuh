@@ -7,6 +7,7 @@
 #include "device.hpp"
 #include "setup.hpp"
 #include "sipg_kernel.cuh"
+#include "sipg_rhs.cuh"
 
 #include <mutex>
 #include <set>
@@ -154,7 +155,63 @@ void launch_d(int K, bool compressed, const dev::ApplyParams<Real> &prm, cudaStr
     }
 }
 
+template <int D, int K, bool C>
+void launch_rhs_one(const dev::RhsParams<double> &prm, cudaStream_t s)
+{
+  using KS = dev::KernelShape<D, K>;
+  const size_t smem = (size_t)KS::SMEM_REALS * sizeof(double);
+  auto kern = dev::sipg_rhs_kernel<double, D, K, C, DGX_BASIS>;
+  static std::set<int> configured;
+  int devid = 0;
+  cuda_check(cudaGetDevice(&devid), "cudaGetDevice");
+  {
+    std::lock_guard<std::mutex> lk(g_mutex);
+    if (!configured.count(devid))
+      {
+        cuda_check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)smem),
+                   "cudaFuncSetAttribute");
+        configured.insert(devid);
+      }
+  }
+  const int grid = (prm.n_tasks + KS::NC - 1) / KS::NC;
+  if (grid > 0)
+    kern<<<grid, KS::THREADS, smem, s>>>(prm);
+  cuda_check(cudaGetLastError(), "sipg_rhs_kernel launch");
+}
+
+template <int D>
+void launch_rhs_d(int K, bool compressed, const dev::RhsParams<double> &prm, cudaStream_t s)
+{
+  switch (K)
+    {
+#define DGX_RHS_K(KK)                                                                      \
+  case KK:                                                                                 \
+    if (compressed)                                                                        \
+      launch_rhs_one<D, KK, true>(prm, s);                                                 \
+    else                                                                                   \
+      launch_rhs_one<D, KK, false>(prm, s);                                                \
+    break;
+#if DGX_BASIS != 2
+      DGX_RHS_K(2) DGX_RHS_K(3)
+#endif
+      DGX_RHS_K(4) DGX_RHS_K(5) DGX_RHS_K(6) DGX_RHS_K(7) DGX_RHS_K(8) DGX_RHS_K(9)
+      DGX_RHS_K(10) DGX_RHS_K(11)
+#undef DGX_RHS_K
+    default: fail(Code::invalid_argument, "assemble_rhs: unsupported k");
+    }
+}
+
 } // namespace
+
+void DGX_FN(launch_rhs)(int D, int K, bool compressed, const dev::RhsParams<double> &prm,
+                        cudaStream_t s)
+{
+  if (D == 2)
+    launch_rhs_d<2>(K, compressed, prm, s);
+  else
+    launch_rhs_d<3>(K, compressed, prm, s);
+}
 
 void DGX_FN(upload_tables)(int K)
 {

@@ -28,5 +28,22 @@ struct ApplyParams
   int n_owned; // slots >= n_owned are ghost cells (ghost-side tasks)
 };
 
+// Right-hand side assembly (assemble_rhs, operators.cpp:266-282): forcing
+// f at the owned cells' quadrature points times det(J) w_q, Dirichlet data g
+// at the computed faces' quadrature points (boundary faces only).
+template <typename Real>
+struct RhsParams
+{
+  const Real *f;    // [slot][q] or null
+  const Real *detw; // [slot][q]
+  const Real *g;    // [local face][qf] or null
+  Real *y;
+  const Real *face_geo;
+  const Real *penalty;
+  const int *task_slot;
+  const int2 *task_face;
+  int n_tasks;
+};
+
 } // namespace dev
 } // namespace dgx

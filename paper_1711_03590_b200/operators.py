@@ -309,6 +309,32 @@ class RankOperator:
                                    y.ctypes.data_as(C.c_void_p)))
         return y
 
+    def quadrature_points(self, which="cells"):
+        """Physical quadrature points: "cells" -> [owned cell, q, d];
+        "faces" -> [computed face, qf, d]; "boundary" -> bool per computed
+        face (operators.cpp:545-560, 1115-1145)."""
+        w = {"cells": 0, "faces": 1, "boundary": 2}[which]
+        n = C.c_int64()
+        check(lib().dgx_get_quadrature_points(self._h, C.c_int(w), None, C.byref(n)))
+        out = np.empty(n.value)
+        check(lib().dgx_get_quadrature_points(self._h, C.c_int(w),
+                                              out.ctypes.data_as(C.c_void_p), C.byref(n)))
+        d = self.config.d
+        lay = self._layout
+        if w == 0:
+            return out.reshape(lay.n_owned_cells, lay.dofs_per_cell, d)
+        if w == 1:
+            return out.reshape(-1, lay.dofs_per_cell // (self.config.p + 1), d)
+        return out.astype(bool)
+
+    def assemble_rhs(self, rhs, forcing=None, dirichlet=None, stream=None):
+        """RankOperator::assemble_rhs (operators.cpp:266-282). forcing /
+        dirichlet: CUDA tensors of f at quadrature_points("cells") and g at
+        quadrature_points("faces") (None: zero); rhs: CUDA tensor of
+        layout().total_size values, overwritten."""
+        check(lib().dgx_assemble_rhs(self._h, _ptr(forcing), _ptr(dirichlet), _ptr(rhs),
+                                     _stream(stream)))
+
     def conjugate_gradient(self, b, x, rel_tol=1e-10, max_iterations=10000, stream=None):
         """conjugate_gradient(make_apply(op), b, x) (solvers.cpp:24-68,189-206)
         on the device; b, x: CUDA tensors of layout().owned_size values.

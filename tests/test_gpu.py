@@ -403,3 +403,133 @@ def test_conjugate_gradient_contract(torch):
     b = torch.ones(n, dtype=torch.float64, device="cuda")
     with pytest.raises(D.DgxInvalidArgument):  # make_apply: single rank only
         op.conjugate_gradient(b, torch.empty_like(b))
+
+
+RHS_CASES = [
+    # d, cells, p, amplitude, m, periodic, ranks, basis
+    (3, [3, 3, 3], 3, 0.05, 2, False, 1, "lagrange_gauss_lobatto"),
+    (2, [4, 5], 4, 0.06, 3, False, 2, "hermite_like"),
+    (3, [4, 4, 3], 5, 0.0, 1, False, 1, "hermite_like"),
+    (3, [3, 3, 4], 2, 0.05, 2, False, 3, "lagrange_gauss"),
+    (3, [2, 3, 4], 6, 0.04, 2, False, 2, "lagrange_gauss_lobatto"),
+]
+_RB = {"lagrange_gauss_lobatto": "gl", "lagrange_gauss": "gauss", "hermite_like": "hermite"}
+
+
+@pytest.mark.parametrize("cfg", RHS_CASES, ids=lambda c: f"d{c[0]}p{c[2]}r{c[6]}-{c[7]}")
+def test_assemble_rhs_against_reference(torch, cfg):
+    """assemble_rhs (forcing + Dirichlet data, operators.cpp:266-282) with the
+    manufactured data of the convergence study, per rank, against the
+    reference; f and g evaluated at the device's quadrature points."""
+    from oracle import reflib as R
+    if not R.available():
+        pytest.skip("reference library not built")
+    D = dgx()
+    d, cells, p, amp, m, periodic, nr, basis = cfg
+    w = R.World(d, cells, p, n_ranks=nr, amplitude=amp, mapping_degree=m, periodic=periodic,
+                basis=_RB[basis], manufactured=True)
+    mesh = D.make_box_mesh(d, cells, amp, periodic, m)
+    faces = D.enumerate_faces(mesh)
+    part = D.partition_cells(mesh, nr)
+    D.assign_face_owners(mesh, faces, part)
+    for r in range(nr):
+        op = D.RankOperator(mesh, part, faces, D.Geometry(source="mesh"),
+                            D.OperatorConfig(d=d, p=p, basis=basis), r)
+        xq = op.quadrature_points("cells")
+        xf = op.quadrature_points("faces")
+        f = torch.tensor(R.manufactured_forcing(d, xq).ravel(), device="cuda")
+        g = torch.tensor(R.manufactured_solution(d, xf).ravel(), device="cuda")
+        rhs = torch.full((op.layout().total_size,), float("nan"), dtype=torch.float64,
+                         device="cuda")
+        op.assemble_rhs(rhs, f, g)
+        torch.cuda.synchronize()
+        ref = w.rhs(r)
+        got = rhs.cpu().numpy()
+        assert rel_linf(got, ref) < TOL64 and rel_l2(got, ref) < TOL64, (rel_linf(got, ref),)
+
+
+def test_quadrature_points_match_reference_geometry(torch):
+    """Face quadrature points equal the reference GeometryCache::face_qpoints
+    (geometry.cpp:415-453) bit for bit on a curved mesh."""
+    from oracle import reflib as R
+    if not R.available():
+        pytest.skip("reference library not built")
+    D = dgx()
+    d, cells, p = 3, [3, 2, 3], 4
+    w = R.World(d, cells, p, amplitude=0.05, mapping_degree=2)
+    mesh = D.make_box_mesh(d, cells, 0.05, False, 2)
+    faces = D.enumerate_faces(mesh)
+    part = D.partition_cells(mesh, 1)
+    D.assign_face_owners(mesh, faces, part)
+    op = D.RankOperator(mesh, part, faces, D.Geometry(source="mesh"),
+                        D.OperatorConfig(d=d, p=p), 0)
+    xf = op.quadrature_points("faces")
+    fids = op.device_geometry(3).astype(np.int64)
+    ref = w.geometry("face_qpoints").reshape(-1, (p + 1) ** (d - 1), d)[fids]
+    assert np.array_equal(xf, ref)
+    bnd = op.quadrature_points("boundary")
+    assert np.array_equal(bnd, faces["exterior_cell"][fids] == D.INVALID_CELL)
+
+
+def _l2_error(op, x, basis, p, d):
+    """|| u_h - u ||_L2 by the k-point Gauss rule (l2_error, bench.cpp:461-520)."""
+    from oracle import oracle as O
+    from oracle import reflib as R
+    S = O.shape_matrices(p, {"lagrange_gauss_lobatto": 0, "lagrange_gauss": 1,
+                             "hermite_like": 2}[basis])["S"]
+    k = p + 1
+    lay = op.layout()
+    c = x[: lay.owned_size].reshape((lay.n_owned_cells,) + (k,) * d)
+    # canonical index: axis 0 fastest -> numpy axes reversed
+    uq = c
+    for a in range(d):
+        ax = d - a  # numpy axis of the cell-local direction a
+        uq = np.moveaxis(np.tensordot(uq, S, axes=([ax], [1])), -1, ax)
+    uq = uq.reshape(lay.n_owned_cells, -1)
+    xq = op.quadrature_points("cells")
+    ue = R.manufactured_solution(d, xq)
+    _, wq = O.gauss(k)
+    w = wq
+    for _ in range(d - 1):
+        w = np.multiply.outer(wq, w)
+    h = 1.0 / round(lay.n_owned_cells ** (1.0 / d))
+    return float(np.sqrt(np.sum((uq - ue) ** 2 * w.reshape(1, -1)) * h ** d))
+
+
+@pytest.mark.parametrize("d,p", [(2, 3), (3, 2)])
+def test_convergence_study(torch, d, p):
+    """The reference convergence study (bench.cpp:525-598) on the device:
+    make_operator_config's basis, Cartesian unit box, manufactured forcing and
+    Dirichlet data through assemble_rhs, device CG to 1e-12; the solution
+    matches the reference CG solution of the same system and the L2 error
+    converges at order p+1."""
+    from oracle import reflib as R
+    if not R.available():
+        pytest.skip("reference library not built")
+    D = dgx()
+    cfg = D.make_operator_config("laplacian", d=d, p=p)
+    errs = []
+    for level in (1, 2, 3):
+        n = 1 << level
+        mesh = D.make_box_mesh(d, n, 0.0, False, 1)
+        faces = D.enumerate_faces(mesh)
+        part = D.partition_cells(mesh, 1)
+        D.assign_face_owners(mesh, faces, part)
+        op = D.RankOperator(mesh, part, faces, D.Geometry(source="mesh"), cfg, 0)
+        xq, xf = op.quadrature_points("cells"), op.quadrature_points("faces")
+        f = torch.tensor(R.manufactured_forcing(d, xq).ravel(), device="cuda")
+        g = torch.tensor(R.manufactured_solution(d, xf).ravel(), device="cuda")
+        b = torch.empty(op.layout().total_size, dtype=torch.float64, device="cuda")
+        op.assemble_rhs(b, f, g)
+        x = torch.empty_like(b)
+        rep = op.conjugate_gradient(b, x, rel_tol=1e-12, max_iterations=100000)
+        assert rep["converged"]
+        w = R.World(d, [n] * d, p, basis=_RB[cfg.basis], manufactured=True)
+        bref = w.rhs(0)
+        assert rel_linf(b.cpu().numpy(), bref) < TOL64
+        xref, rref = w.cg(bref, 1e-12, 100000)
+        assert rref["converged"]
+        assert rel_l2(x.cpu().numpy(), xref) < 1e-9
+        errs.append(_l2_error(op, x.cpu().numpy(), cfg.basis, p, d))
+    rates = [np.log2(errs[i] / errs[i + 1]) for i in range(len(errs) - 1)]
+    assert rates[-1] > p + 0.5, (errs, rates)
