@@ -105,6 +105,8 @@ typedef struct dgx_geometry
   int compressed;                /* HOST_ARRAYS: GeometryCache::compressed() */
   const double *inv_jac_t, *jxw; /* HOST_ARRAYS, [cell][q][d*d], [cell][q] */
   const double *face_jxw, *face_jni, *face_jne, *penalty; /* HOST_ARRAYS */
+  const double *face_normal; /* HOST_ARRAYS, advection: GeometryCache::face_normal
+                                [face][qf][d] */
 } dgx_geometry;
 
 /* Replaces dg::OperatorConfig (operators.hpp:26-51) for this path: the
@@ -120,6 +122,12 @@ typedef struct dgx_config
                            make_operator_config, operators.cpp:27-41) */
   int geometry_variant; /* 3: g3 (others rejected) */
   int precision;        /* 0: fp64, 1: fp32 */
+  int kind;             /* OperatorKind: 0 laplacian, 1 advection (fp64, nodal or
+                           Lagrange-Gauss basis) */
+  double velocity[3];   /* advection: VelocityField::constant */
+  int variable_velocity; /* advection: 1 = VelocityField::field, values given per
+                            quadrature point by dgx_set_velocity (no Cartesian
+                            compression, geometry.cpp:267-271) */
 } dgx_config;
 
 /* Replaces the RankOperator constructor arguments (operators.hpp:72-75):
@@ -176,6 +184,13 @@ dgx_status dgx_get_plan_dofs(const dgx_op *op, int which, int idx, uint32_t *dof
  * which=3 gives their global ids); 2: boundary flag (0/1) per computed face.
  * Pass out=NULL to query n. */
 dgx_status dgx_get_quadrature_points(dgx_op *op, int which, double *out, int64_t *n);
+/* Advection with a variable velocity: c at the owned cells' quadrature points
+ * [cell][q][d] and at the computed faces' quadrature points [face][qf][d]
+ * (device arrays, dgx_get_quadrature_points order); replaces the field
+ * evaluation of load_cell_geometry / load_face_geometry (operators.cpp:
+ * 397-545). Also accepted for a constant velocity config (overrides it). */
+dgx_status dgx_set_velocity(dgx_op *op, const double *c_cells, const double *c_faces,
+                            void *stream);
 /* RankOperator::assemble_rhs (operators.cpp:266-282): rhs = forcing
  * (f det(J) w_q tested with the basis, :1115-1145) + the Dirichlet data moved
  * to the right-hand side by the boundary faces (:1033-1111). f: device

@@ -53,12 +53,16 @@ public:
                const dg::OperatorConfig &config, int rank, int device = 0)
     : cfg_(config), geom_(std::move(geometry))
   {
-    if (config.kind != dg::OperatorKind::laplacian)
-      throw std::invalid_argument("dgx_ref::RankOperator: Laplacian only");
+    if (config.kind != dg::OperatorKind::laplacian &&
+        config.kind != dg::OperatorKind::advection)
+      throw std::invalid_argument("dgx_ref::RankOperator: Laplacian or advection only");
+    if (config.kind == dg::OperatorKind::advection && !config.velocity.is_constant())
+      throw std::invalid_argument(
+        "dgx_ref::RankOperator: pass a variable velocity through dgx_set_velocity");
     if (mesh.d != config.d)
       throw std::invalid_argument("RankOperator: mesh dimension mismatch");
     if (!geom_ || geom_->k != config.k() || geom_->l != config.k() ||
-        geom_->equation != dg::Equation::laplacian ||
+        geom_->equation != config.equation() ||
         geom_->variant != dg::GeometryVariant::g3)
       throw std::invalid_argument(
         "RankOperator: geometry cache does not match the configuration");
@@ -93,9 +97,12 @@ public:
     s.config.d = config.d;
     s.config.p = config.p;
     s.config.W = 1;
-    s.config.basis = config.basis == dg::BasisKind::lagrange_gauss_lobatto ? 0 : -1;
+    s.config.basis = static_cast<int>(config.basis); // BasisKind order (basis.hpp:10-15)
     s.config.geometry_variant = 3;
     s.config.precision = 0;
+    s.config.kind = config.kind == dg::OperatorKind::advection ? 1 : 0;
+    for (int a = 0; a < 3; ++a)
+      s.config.velocity[a] = config.velocity.constant[a];
     s.geometry.source = DGX_GEOMETRY_HOST_ARRAYS;
     s.geometry.compressed = geom_->compressed() ? 1 : 0;
     s.geometry.inv_jac_t = geom_->inv_jac_t.data();
@@ -104,6 +111,7 @@ public:
     s.geometry.face_jni = geom_->face_jni.data();
     s.geometry.face_jne = geom_->face_jne.data();
     s.geometry.penalty = geom_->penalty.data();
+    s.geometry.face_normal = geom_->face_normal.data();
     check(dgx_create(&s, device, &op_));
     layout_ = dg::build_dof_layout(mesh, partition, faces, rank, config.k(), 1);
   }

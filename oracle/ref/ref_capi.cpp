@@ -42,6 +42,16 @@ namespace
 thread_local std::string g_err;
 thread_local int g_basis = 0; // BasisKind for new worlds; -1 = reference default
 thread_local int g_manufactured = 0; // forcing/dirichlet of the convergence study
+thread_local int g_kind = 0;          // 0 laplacian, 1 advection
+thread_local double g_velocity[3] = {1, 1, 1};
+thread_local int g_velocity_field = 0; // 1: the variable test field below
+
+// Variable transport field used by the advection tests (test input).
+std::array<double, 3> test_velocity(const std::array<double, 3> &x)
+{
+  return {1.0 + 0.3 * std::sin(2.0 * M_PI * x[1]), 0.7 + 0.2 * std::cos(2.0 * M_PI * x[0]),
+          0.4 + 0.1 * x[0] * x[1]};
+}
 
 // The manufactured solution of the reference convergence study
 // (bench.cpp:437-459), restated here as test input.
@@ -52,6 +62,14 @@ double mf_solution(int d, const std::array<double, 3> &x)
   if (d == 3)
     u *= std::cos(1.1 * x[2] + 0.1);
   return u;
+}
+std::array<double, 3> mf_gradient(int d, const std::array<double, 3> &x)
+{
+  const double c0 = std::cos(2.3 * x[0] + 0.4), s0 = std::sin(2.3 * x[0] + 0.4);
+  const double c1 = std::cos(1.7 * x[1] - 0.2), s1 = std::sin(1.7 * x[1] - 0.2);
+  const double c2 = d == 3 ? std::cos(1.1 * x[2] + 0.1) : 1.0;
+  const double s2 = d == 3 ? std::sin(1.1 * x[2] + 0.1) : 0.0;
+  return {-2.3 * s0 * c1 * c2, -1.7 * c0 * s1 * c2, d == 3 ? -1.1 * c0 * c1 * s2 : 0.0};
 }
 double mf_neg_laplacian(int d, const std::array<double, 3> &x)
 {
@@ -125,14 +143,32 @@ World *make_world_common(int d, const int *cells, double amplitude,
   w->mesh = build_mesh(d, {cells[0], cells[1], d > 2 ? cells[2] : 1},
                        {0, 0, 0}, {1, 1, 1}, amplitude, mapping_degree,
                        boundary);
-  w->cfg = make_operator_config(OperatorKind::laplacian, d, p, W,
-                                GeometryVariant::g3);
+  const OperatorKind kind = g_kind == 1 ? OperatorKind::advection : OperatorKind::laplacian;
+  w->cfg = make_operator_config(kind, d, p, W, GeometryVariant::g3);
   if (g_basis >= 0)
     w->cfg.basis = static_cast<BasisKind>(g_basis); // GL unless selected
+  if (kind == OperatorKind::advection)
+    {
+      w->cfg.velocity.constant = {g_velocity[0], g_velocity[1], g_velocity[2]};
+      if (g_velocity_field == 1)
+        w->cfg.velocity.field = test_velocity;
+    }
   if (g_manufactured)
     {
       w->cfg.dirichlet = [d](const std::array<double, 3> &x) { return mf_solution(d, x); };
-      w->cfg.forcing = [d](const std::array<double, 3> &x) { return mf_neg_laplacian(d, x); };
+      if (kind == OperatorKind::laplacian)
+        w->cfg.forcing = [d](const std::array<double, 3> &x) { return mf_neg_laplacian(d, x); };
+      else
+        {
+          const VelocityField vel = w->cfg.velocity;
+          w->cfg.forcing = [d, vel](const std::array<double, 3> &x) {
+            const std::array<double, 3> g = mf_gradient(d, x), c = vel(x);
+            double f = 0;
+            for (int a = 0; a < d; ++a)
+              f += c[a] * g[a];
+            return f;
+          };
+        }
     }
   w->faces = enumerate_faces(w->mesh);
   w->partition = partition_cells(w->mesh, n_ranks);
@@ -176,6 +212,21 @@ int dgref_set_basis(int kind)
     if (kind < -1 || kind > 2)
       throw std::invalid_argument("dgref_set_basis: unknown basis kind");
     g_basis = kind;
+  });
+}
+
+// Operator of the worlds created next: kind 0 Laplacian, 1 advection with the
+// constant velocity c (field 1: the variable test field above).
+int dgref_set_operator(int kind, const double *c, int field)
+{
+  return guard([&] {
+    if (kind != 0 && kind != 1)
+      throw std::invalid_argument("dgref_set_operator: unknown kind");
+    g_kind = kind;
+    if (c)
+      for (int a = 0; a < 3; ++a)
+        g_velocity[a] = c[a];
+    g_velocity_field = field;
   });
 }
 

@@ -55,6 +55,24 @@ def manufactured_solution(d, x):
     return u
 
 
+def manufactured_gradient(d, x):
+    """exact_gradient (bench.cpp:446-453), [..., d]."""
+    c0, s0 = np.cos(2.3 * x[..., 0] + 0.4), np.sin(2.3 * x[..., 0] + 0.4)
+    c1, s1 = np.cos(1.7 * x[..., 1] - 0.2), np.sin(1.7 * x[..., 1] - 0.2)
+    if d == 3:
+        c2, s2 = np.cos(1.1 * x[..., 2] + 0.1), np.sin(1.1 * x[..., 2] + 0.1)
+        return np.stack([-2.3 * s0 * c1 * c2, -1.7 * c0 * s1 * c2, -1.1 * c0 * c1 * s2], -1)
+    return np.stack([-2.3 * s0 * c1, -1.7 * c0 * s1], -1)
+
+
+def test_velocity(d, x):
+    """The harness's variable transport field (ref_capi.cpp test_velocity)."""
+    c = np.stack([1.0 + 0.3 * np.sin(2.0 * np.pi * x[..., 1]),
+                  0.7 + 0.2 * np.cos(2.0 * np.pi * x[..., 0]),
+                  0.4 + 0.1 * x[..., 0] * x[..., 1]], -1)
+    return c[..., :d]
+
+
 def manufactured_forcing(d, x):
     """exact_neg_laplacian (bench.cpp:455-459)."""
     lam = 2.3 * 2.3 + 1.7 * 1.7 + (1.1 * 1.1 if d == 3 else 0.0)
@@ -117,16 +135,24 @@ class World:
 
     def __init__(self, d, cells, p, n_ranks=1, amplitude=0.0,
                  mapping_degree=1, periodic=False, W=1, geometry=None, basis="gl",
-                 manufactured=False):
+                 manufactured=False, kind="laplacian", velocity=(1.0, 1.0, 1.0),
+                 velocity_field=0):
         """manufactured: forcing / Dirichlet data of the reference convergence
-        study (bench.cpp:437-560) for rhs()."""
+        study (bench.cpp:437-560) for rhs(). kind "advection": the transport
+        operator with a constant velocity, or velocity_field=1 (the harness's
+        variable test field)."""
         _chk(lib().dgref_set_manufactured(C.c_int(int(manufactured))))
+        vel = (C.c_double * 3)(*velocity)
+        _chk(lib().dgref_set_operator(C.c_int(1 if kind == "advection" else 0), vel,
+                                      C.c_int(velocity_field)))
+        self.kind = kind
         try:
             with _basis(basis):
                 self._create(d, cells, p, n_ranks, amplitude, mapping_degree, periodic, W,
                              geometry)
         finally:
             lib().dgref_set_manufactured(C.c_int(0))
+            lib().dgref_set_operator(C.c_int(0), None, C.c_int(0))
 
     def _create(self, d, cells, p, n_ranks, amplitude, mapping_degree, periodic, W,
                 geometry):

@@ -59,13 +59,15 @@ class CGeometry(C.Structure):
                 ("cartesian", C.c_int), ("compressed", C.c_int),
                 ("inv_jac_t", C.c_void_p), ("jxw", C.c_void_p),
                 ("face_jxw", C.c_void_p), ("face_jni", C.c_void_p),
-                ("face_jne", C.c_void_p), ("penalty", C.c_void_p)]
+                ("face_jne", C.c_void_p), ("penalty", C.c_void_p),
+                ("face_normal", C.c_void_p)]
 
 
 class CConfig(C.Structure):
     _fields_ = [("d", C.c_int), ("p", C.c_int), ("W", C.c_int),
                 ("basis", C.c_int), ("geometry_variant", C.c_int),
-                ("precision", C.c_int)]
+                ("precision", C.c_int), ("kind", C.c_int), ("velocity", C.c_double * 3),
+                ("variable_velocity", C.c_int)]
 
 
 class CSetup(C.Structure):
@@ -111,7 +113,7 @@ EXPORTS = [
     "dgx_create", "dgx_destroy", "dgx_get_layout", "dgx_get_ghost_cells",
     "dgx_get_plan", "dgx_get_plan_dofs", "dgx_apply", "dgx_apply_f32", "dgx_apply_host",
     "dgx_apply_phase", "dgx_accumulate_plan", "dgx_conjugate_gradient",
-    "dgx_get_quadrature_points", "dgx_assemble_rhs", "dgx_nccl_unique_id",
+    "dgx_get_quadrature_points", "dgx_assemble_rhs", "dgx_set_velocity", "dgx_nccl_unique_id",
     "dgx_exchanger_create", "dgx_exchanger_hooks", "dgx_exchanger_destroy",
     "dgx_get_geometry", "dgx_get_tasks", "dgx_get_stats", "dgx_random_uniform",
 ]

@@ -268,6 +268,14 @@ dgx_status dgx_get_quadrature_points(dgx_op *op, int which, double *out, int64_t
   });
 }
 
+dgx_status dgx_set_velocity(dgx_op *op, const double *c_cells, const double *c_faces,
+                            void *stream)
+{
+  return guard([&] {
+    op_of(op).set_velocity(c_cells, c_faces, static_cast<cudaStream_t>(stream));
+  });
+}
+
 dgx_status dgx_assemble_rhs(dgx_op *op, const double *f, const double *g, double *rhs,
                             void *stream)
 {

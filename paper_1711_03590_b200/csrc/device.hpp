@@ -88,6 +88,8 @@ template <typename Real>
 struct ApplyParams;
 template <typename Real>
 struct RhsParams;
+template <typename Real>
+struct AdvParams;
 }
 
 // sipg.cu (kernels in sipg_gl.cu / sipg_gauss.cu / sipg_hermite.cu);
@@ -97,8 +99,18 @@ int kernel_cells_per_cta(int D, int K);
 template <typename Real>
 void launch_apply(int D, int K, int basis, bool compressed, const dev::ApplyParams<Real> &prm,
                   cudaStream_t s);
-void launch_rhs(int D, int K, int basis, bool compressed, const dev::RhsParams<double> &prm,
+void launch_rhs(int D, int K, int basis, bool compressed, bool adv,
+                const dev::RhsParams<double> &prm, cudaStream_t s);
+void launch_adv(int D, int K, int basis, bool compressed, const dev::AdvParams<double> &prm,
                 cudaStream_t s);
+// advection.cu: cell coefficient J^{-1} c det(J) w [geo][d][q] (or [geo][d]
+// compressed) and face records (JxW_f, c.n) [face][2][qf] (or [face][2]) from
+// the g3 arrays, the unit normals and the velocity (constant, or per point)
+void run_adv_coefficients(int d, int k, bool compressed, long long n_cells, long long n_faces,
+                          const double *cell_geo, const double *face_geo,
+                          const double *normals, const double velocity[3],
+                          const double *c_cells, const double *c_faces, double *adv_cell,
+                          double *adv_face, cudaStream_t s);
 
 // geometry.cu -- device precompute of the g3 arrays from mapping support
 // points (reference geometry.cpp:36-150,248-522), written straight into the
@@ -118,6 +130,7 @@ struct GeometryJob
   double *face_geo = nullptr;  // [n_faces][2d+1][k^{d-1}]
   double *penalty = nullptr;   // [n_faces]
   double *volume = nullptr;    // scratch [n_slots]
+  double *face_normal = nullptr; // optional [n_faces][d][k^{d-1} or 1] unit normals (e-)
 };
 void run_geometry(const GeometryJob &job, cudaStream_t s);
 // physical quadrature points of the owned cells ([cell][q][d]) with the

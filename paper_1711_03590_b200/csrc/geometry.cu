@@ -273,6 +273,9 @@ __global__ void face_geometry_kernel(GeometryJob job, GeoConst gc, int *bad)
       nrm = sqrt(nrm);
       for (int i = 0; i < d; ++i)
         normal[i] = sign * nvec[i] / nrm;
+      if (job.face_normal && (!job.compress || q == 0))
+        for (int i = 0; i < d; ++i)
+          job.face_normal[(f * d + i) * nrf + q] = normal[i];
       const double jxw_f = det * nrm * wqf;
       if (!job.compress)
         fg[q] = jxw_f;

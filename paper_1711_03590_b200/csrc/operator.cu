@@ -54,6 +54,20 @@ Operator::Operator(const dgx_setup &s, int device) : device_(device)
   if (c.basis == 2 && c.p < 3)
     fail(Code::invalid_argument, "RankOperator: the Hermite-type basis needs degree >= 3");
   basis_ = c.basis;
+  if (c.kind != 0 && c.kind != 1)
+    fail(Code::invalid_argument, "RankOperator: unknown operator kind");
+  kind_ = c.kind;
+  if (kind_ == 1)
+    {
+      if (c.precision != 0)
+        fail(Code::invalid_argument, "RankOperator: advection runs in fp64 only");
+      if (c.basis == 2)
+        fail(Code::invalid_argument,
+             "RankOperator: advection with the Hermite-like basis is not implemented");
+      for (int a = 0; a < 3; ++a)
+        velocity_[a] = c.velocity[a];
+      variable_velocity_ = c.variable_velocity != 0;
+    }
   precision_ = c.precision;
   nq_ = 1;
   for (int a = 0; a < d_; ++a)
@@ -89,13 +103,15 @@ Operator::Operator(const dgx_setup &s, int device) : device_(device)
   else
     part = make_partition(mesh_, faces, s.n_ranks);
   n_ranks_ = part.n_ranks;
-  layout_ = build_layout(mesh_, faces, part, s.rank, k_, basis_);
+  layout_ = build_layout(mesh_, faces, part, s.rank, k_, basis_, kind_);
 
   build_tasks(faces, part);
   if (host_only_)
     return;
   build_geometry(s, faces);
   upload_tables(k_, basis_);
+  if (kind_ == 1)
+    set_velocity(nullptr, nullptr, nullptr);
 }
 
 // Task lists. Owned cells whose computed faces never read a ghost form the
@@ -362,6 +378,23 @@ void Operator::build_geometry(const dgx_setup &s, const std::vector<RawFace> &fa
       cell_geo_.upload(cg);
       face_geo_.upload(fg);
       penalty_.upload(pen);
+      if (kind_ == 1)
+        {
+          if (!g.face_normal)
+            fail(Code::invalid_argument, "geometry: advection needs the face normals");
+          if (compressed_ && variable_velocity_)
+            fail(Code::invalid_argument,
+                 "geometry: a variable velocity needs an uncompressed geometry cache");
+          std::vector<double> nv((size_t)nmy * d_ * nrf);
+          for (long long i = 0; i < nmy; ++i)
+            {
+              const long long f = layout_.my_faces[i];
+              for (long long q = 0; q < nrf; ++q)
+                for (int b = 0; b < d_; ++b)
+                  nv[(i * d_ + b) * nrf + q] = g.face_normal[(f * nqf_ + q) * d_ + b];
+            }
+          normals_.upload(nv);
+        }
     }
   else
     {
@@ -401,7 +434,7 @@ void Operator::build_geometry(const dgx_setup &s, const std::vector<RawFace> &fa
         }
       if (g.coefficient != 0 && g.coefficient != 1)
         fail(Code::invalid_argument, "geometry: unknown coefficient");
-      compressed_ = cartesian && !g.coefficient;
+      compressed_ = cartesian && !g.coefficient && !variable_velocity_;
       DeviceArray<double> &dsup = support_;
       dsup.upload(support);
       has_mapping_ = true;
@@ -442,6 +475,11 @@ void Operator::build_geometry(const dgx_setup &s, const std::vector<RawFace> &fa
       job.face_geo = face_geo_.get();
       job.penalty = penalty_.get();
       job.volume = vol.get();
+      if (kind_ == 1)
+        {
+          normals_.resize((size_t)nmy * d_ * (compressed_ ? 1 : nqf_));
+          job.face_normal = normals_.get();
+        }
       run_geometry(job, nullptr);
     }
   if (precision_ == 1)
@@ -457,11 +495,52 @@ void Operator::build_geometry(const dgx_setup &s, const std::vector<RawFace> &fa
   cuda_check(cudaDeviceSynchronize(), "geometry setup");
 }
 
+void Operator::set_velocity(const double *c_cells, const double *c_faces, cudaStream_t s)
+{
+  if (kind_ != 1)
+    fail(Code::invalid_argument, "set_velocity: not an advection operator");
+  if (host_only_)
+    return;
+  if (compressed_ && (c_cells || c_faces))
+    fail(Code::invalid_argument,
+         "set_velocity: per-point velocities need variable_velocity = 1 (uncompressed geometry)");
+  if (variable_velocity_ && (!c_cells || !c_faces) && adv_cell_.size() > 0)
+    fail(Code::invalid_argument, "set_velocity: missing per-point velocity arrays");
+  cuda_check(cudaSetDevice(device_), "cudaSetDevice");
+  const long long nrec = compressed_ ? 1 : nq_, nrf = compressed_ ? 1 : nqf_;
+  const long long nmy = (long long)layout_.my_faces.size();
+  adv_cell_.resize((size_t)layout_.n_owned * d_ * nrec);
+  adv_face_.resize((size_t)nmy * 2 * nrf);
+  run_adv_coefficients(d_, k_, compressed_, layout_.n_owned, nmy, cell_geo_.get(),
+                       face_geo_.get(), normals_.get(), velocity_, c_cells, c_faces,
+                       adv_cell_.get(), adv_face_.get(), s);
+}
+
 template <typename Real>
 void Operator::launch_range(int begin, int count, const Real *u, Real *y, cudaStream_t s)
 {
   if (count <= 0)
     return;
+  if (kind_ == 1)
+    {
+      if constexpr (sizeof(Real) == 8)
+        {
+          dev::AdvParams<double> ap;
+          ap.u = u;
+          ap.y = y;
+          ap.cell = adv_cell_.get();
+          ap.face = adv_face_.get();
+          ap.task_slot = task_slot_.get() + begin;
+          ap.task_geo = task_geo_.get() + begin;
+          ap.task_face = task_face_.get() + (long long)begin * 2 * d_;
+          ap.n_tasks = count;
+          ap.n_owned = static_cast<int>(layout_.n_owned);
+          launch_adv(d_, k_, basis_, compressed_, ap, s);
+        }
+      else
+        fail(Code::invalid_argument, "advection: fp64 only");
+      return;
+    }
   dev::ApplyParams<Real> prm;
   prm.u = u;
   prm.y = y;
@@ -632,12 +711,12 @@ void Operator::assemble_rhs(const double *f, const double *g, double *rhs, cudaS
   prm.detw = cell_detw_.get();
   prm.g = g;
   prm.y = rhs;
-  prm.face_geo = face_geo_.get();
+  prm.face_geo = kind_ == 1 ? adv_face_.get() : face_geo_.get();
   prm.penalty = penalty_.get();
   prm.task_slot = task_slot_.get();
   prm.task_face = task_face_.get();
   prm.n_tasks = static_cast<int>(layout_.n_owned); // owned tasks come first
-  launch_rhs(d_, k_, basis_, compressed_, prm, s);
+  launch_rhs(d_, k_, basis_, compressed_, kind_ == 1, prm, s);
 }
 
 std::vector<double> Operator::geometry(int which) const

@@ -28,6 +28,9 @@ public:
   int k() const { return k_; }
   int precision() const { return precision_; }
   int basis() const { return basis_; }
+  int kind() const { return kind_; }
+  // advection: velocity per quadrature point (device [cell][q][d], [face][qf][d])
+  void set_velocity(const double *c_cells, const double *c_faces, cudaStream_t s);
   int device() const { return device_; }
   int n_ranks() const { return n_ranks_; }
   long long nq() const { return nq_; }
@@ -66,6 +69,11 @@ private:
 
   MeshDesc mesh_;
   int d_ = 3, p_ = 1, k_ = 2, precision_ = 0, device_ = 0, n_ranks_ = 1, basis_ = 0;
+  int kind_ = 0; // 0 Laplacian, 1 advection
+  double velocity_[3] = {1, 1, 1};
+  bool variable_velocity_ = false;
+  DeviceArray<double> normals_;           // advection: [face][d][qf or 1]
+  DeviceArray<double> adv_cell_, adv_face_; // advection records
   long long nq_ = 0, nqf_ = 0;
   RankLayout layout_;
   bool compressed_ = false;

@@ -534,7 +534,7 @@ long long RankLayout::slot(std::uint32_t g) const
 }
 
 RankLayout build_layout(const MeshDesc &m, const std::vector<RawFace> &faces,
-                        const Partition &p, int rank, int k, int basis)
+                        const Partition &p, int rank, int k, int basis, int kind)
 {
   if (rank < 0 || rank >= p.n_ranks)
     fail(Code::invalid_argument, "build_dof_layout: rank out of range");
@@ -569,7 +569,9 @@ RankLayout build_layout(const MeshDesc &m, const std::vector<RawFace> &faces,
   // owned elsewhere than the face contributes that cell, with the dofs the
   // face evaluation reads (mark_face_dofs, :46-70): two layers next to the
   // face for the Hermite-like basis, the whole cell otherwise
-  const int nl = basis == 2 ? 2 : 0;
+  // one layer for values on a nodal basis, two for the Hermite-like basis,
+  // the whole cell otherwise (mark_face_dofs, ghost_exchange.cpp:46-70)
+  const int nl = basis == 2 ? 2 : (basis == 0 && kind == 1 ? 1 : 0);
   auto mark = [&](std::vector<char> &mask, int face_number) {
     if (mask.empty())
       mask.assign((size_t)dpc, 0);

@@ -159,8 +159,10 @@ struct RankLayout
   long long slot(std::uint32_t global) const;
 };
 
+// kind: 0 Laplacian (values and first derivatives), 1 advection (values):
+// ghost_need, ghost_exchange.cpp:13-24
 RankLayout build_layout(const MeshDesc &m, const std::vector<RawFace> &faces,
-                        const Partition &p, int rank, int k, int basis);
+                        const Partition &p, int rank, int k, int basis, int kind = 0);
 
 // Mapping support points [cell][(m+1)^d][d] on Gauss-Lobatto nodes of
 // degree m for the listed global cells (build_mapping, geometry.cpp:36-63,

@@ -9,7 +9,9 @@ namespace dgx
 
 #define DGX_DECL(B)                                                                       \
   void upload_tables_##B(int K);                                                         \
-  void launch_rhs_##B(int D, int K, bool compressed, const dev::RhsParams<double> &prm,   \
+  void launch_rhs_##B(int D, int K, bool compressed, bool adv,                           \
+                      const dev::RhsParams<double> &prm, cudaStream_t s);                \
+  void launch_adv_##B(int D, int K, bool compressed, const dev::AdvParams<double> &prm,   \
                       cudaStream_t s);                                                   \
   template <typename Real>                                                               \
   void launch_apply_##B(int D, int K, bool compressed, const dev::ApplyParams<Real> &prm, \
@@ -56,14 +58,26 @@ void launch_apply(int D, int K, int basis, bool compressed, const dev::ApplyPara
     }
 }
 
-void launch_rhs(int D, int K, int basis, bool compressed, const dev::RhsParams<double> &prm,
+void launch_rhs(int D, int K, int basis, bool compressed, bool adv,
+                const dev::RhsParams<double> &prm, cudaStream_t s)
+{
+  switch (basis)
+    {
+    case 0: launch_rhs_gl(D, K, compressed, adv, prm, s); break;
+    case 1: launch_rhs_gauss(D, K, compressed, adv, prm, s); break;
+    case 2: launch_rhs_hermite(D, K, compressed, adv, prm, s); break;
+    default: fail(Code::invalid_argument, "unknown basis kind");
+    }
+}
+
+void launch_adv(int D, int K, int basis, bool compressed, const dev::AdvParams<double> &prm,
                 cudaStream_t s)
 {
   switch (basis)
     {
-    case 0: launch_rhs_gl(D, K, compressed, prm, s); break;
-    case 1: launch_rhs_gauss(D, K, compressed, prm, s); break;
-    case 2: launch_rhs_hermite(D, K, compressed, prm, s); break;
+    case 0: launch_adv_gl(D, K, compressed, prm, s); break;
+    case 1: launch_adv_gauss(D, K, compressed, prm, s); break;
+    case 2: launch_adv_hermite(D, K, compressed, prm, s); break;
     default: fail(Code::invalid_argument, "unknown basis kind");
     }
 }

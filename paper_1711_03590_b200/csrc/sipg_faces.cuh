@@ -115,7 +115,6 @@ __device__ __forceinline__ void face_axis_v4(const ApplyParams<Real> &prm, Real 
 #pragma unroll
       for (int s = 0; s < 2; ++s)
         {
-          const int me = s == 0 ? K - 1 : 0, mi = s == 0 ? K - 2 : 1;
           xe[s] = xi[s] = Real(0);
           if (tf[s].x >= 0)
             {

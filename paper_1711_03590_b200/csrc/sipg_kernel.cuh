@@ -204,16 +204,16 @@ __device__ __forceinline__ Real hsign(int j)
   return j == K - 2 ? Real(-1) : Real(1);
 }
 
-// Dofs of a ghost cell that a face evaluation of the Hermite-like basis may
-// read (two layers next to every face this rank computes for it,
-// read_face_dofs / mark_face_dofs, dof_layout.hpp:291-336,
-// ghost_exchange.cpp:46-70): bit m set if the dof (thread pencil p, index m
-// along axis D-1) is one of them. Ghost data outside these layers is never
-// shipped and must not be read.
-template <int D, int K>
-__device__ __forceinline__ unsigned hermite_ghost_mask(const int2 *tf, int p)
+// Dofs of a ghost cell that a face evaluation may read: NLAY layers next to
+// every face this rank computes for it (two for the Hermite-like basis, one
+// for values on a nodal basis; read_face_dofs / mark_face_dofs,
+// dof_layout.hpp:291-336, ghost_exchange.cpp:46-70): bit m set if the dof
+// (thread pencil p, index m along axis D-1) is one of them. Ghost data
+// outside these layers is never shipped and must not be read.
+template <int D, int K, int NLAY>
+__device__ __forceinline__ unsigned ghost_layer_mask(const int2 *tf, int p)
 {
-  constexpr unsigned ALL = (1u << K) - 1u;
+  constexpr unsigned ALL = (1u << K) - 1u, LOW = (1u << NLAY) - 1u;
   unsigned keep = 0;
 #pragma unroll
   for (int phi = 0; phi < 2 * D; ++phi)
@@ -222,11 +222,11 @@ __device__ __forceinline__ unsigned hermite_ghost_mask(const int2 *tf, int p)
         continue;
       const int a = phi / 2, side = phi % 2;
       if (a == D - 1)
-        keep |= side == 0 ? 3u : (3u << (K - 2));
+        keep |= side == 0 ? LOW : (LOW << (K - NLAY));
       else
         {
           const int c = (D == 2 || a == 0) ? p % K : p / K;
-          if (side == 0 ? c < 2 : c >= K - 2)
+          if (side == 0 ? c < NLAY : c >= K - NLAY)
             keep = ALL;
         }
     }
@@ -498,7 +498,7 @@ __global__ void __launch_bounds__(KernelShape<D, K>::THREADS, KernelShape<D, K>:
 #pragma unroll
           for (int phi = 0; phi < 2 * D; ++phi)
             tf[phi] = prm.task_face[task * 2 * D + phi];
-          gmask = hermite_ghost_mask<D, K>(tf, p);
+          gmask = ghost_layer_mask<D, K, 2>(tf, p);
         }
     }
 

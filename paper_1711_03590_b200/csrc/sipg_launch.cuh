@@ -8,6 +8,7 @@
 #include "setup.hpp"
 #include "sipg_kernel.cuh"
 #include "sipg_rhs.cuh"
+#include "sipg_adv.cuh"
 
 #include <mutex>
 #include <set>
@@ -155,12 +156,63 @@ void launch_d(int K, bool compressed, const dev::ApplyParams<Real> &prm, cudaStr
     }
 }
 
+template <typename KERN>
+void set_smem_once(KERN kern, size_t smem, std::set<int> &configured)
+{
+  int devid = 0;
+  cuda_check(cudaGetDevice(&devid), "cudaGetDevice");
+  std::lock_guard<std::mutex> lk(g_mutex);
+  if (!configured.count(devid))
+    {
+      cuda_check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)smem),
+                 "cudaFuncSetAttribute");
+      cuda_check(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                      cudaSharedmemCarveoutMaxShared),
+                 "cudaFuncSetAttribute(carveout)");
+      configured.insert(devid);
+    }
+}
+
 template <int D, int K, bool C>
+void launch_adv_one(const dev::AdvParams<double> &prm, cudaStream_t s)
+{
+  using KS = dev::KernelShape<D, K>;
+  const size_t smem = (size_t)KS::SMEM_REALS * sizeof(double);
+  auto kern = dev::sipg_adv_kernel<double, D, K, C, DGX_BASIS>;
+  static std::set<int> configured;
+  set_smem_once(kern, smem, configured);
+  const int grid = (prm.n_tasks + KS::NC - 1) / KS::NC;
+  if (grid > 0)
+    kern<<<grid, KS::THREADS, smem, s>>>(prm);
+  cuda_check(cudaGetLastError(), "sipg_adv_kernel launch");
+}
+
+template <int D>
+void launch_adv_d(int K, bool compressed, const dev::AdvParams<double> &prm, cudaStream_t s)
+{
+  switch (K)
+    {
+#define DGX_ADV_K(KK)                                                                      \
+  case KK:                                                                                 \
+    if (compressed)                                                                        \
+      launch_adv_one<D, KK, true>(prm, s);                                                 \
+    else                                                                                   \
+      launch_adv_one<D, KK, false>(prm, s);                                                \
+    break;
+      DGX_ADV_K(2) DGX_ADV_K(3) DGX_ADV_K(4) DGX_ADV_K(5) DGX_ADV_K(6) DGX_ADV_K(7)
+      DGX_ADV_K(8) DGX_ADV_K(9) DGX_ADV_K(10) DGX_ADV_K(11)
+#undef DGX_ADV_K
+    default: fail(Code::invalid_argument, "advection: unsupported k");
+    }
+}
+
+template <int D, int K, bool C, bool ADV>
 void launch_rhs_one(const dev::RhsParams<double> &prm, cudaStream_t s)
 {
   using KS = dev::KernelShape<D, K>;
   const size_t smem = (size_t)KS::SMEM_REALS * sizeof(double);
-  auto kern = dev::sipg_rhs_kernel<double, D, K, C, DGX_BASIS>;
+  auto kern = dev::sipg_rhs_kernel<double, D, K, C, DGX_BASIS, ADV>;
   static std::set<int> configured;
   int devid = 0;
   cuda_check(cudaGetDevice(&devid), "cudaGetDevice");
@@ -180,7 +232,7 @@ void launch_rhs_one(const dev::RhsParams<double> &prm, cudaStream_t s)
   cuda_check(cudaGetLastError(), "sipg_rhs_kernel launch");
 }
 
-template <int D>
+template <int D, bool ADV>
 void launch_rhs_d(int K, bool compressed, const dev::RhsParams<double> &prm, cudaStream_t s)
 {
   switch (K)
@@ -188,9 +240,9 @@ void launch_rhs_d(int K, bool compressed, const dev::RhsParams<double> &prm, cud
 #define DGX_RHS_K(KK)                                                                      \
   case KK:                                                                                 \
     if (compressed)                                                                        \
-      launch_rhs_one<D, KK, true>(prm, s);                                                 \
+      launch_rhs_one<D, KK, true, ADV>(prm, s);                                            \
     else                                                                                   \
-      launch_rhs_one<D, KK, false>(prm, s);                                                \
+      launch_rhs_one<D, KK, false, ADV>(prm, s);                                           \
     break;
 #if DGX_BASIS != 2
       DGX_RHS_K(2) DGX_RHS_K(3)
@@ -204,13 +256,36 @@ void launch_rhs_d(int K, bool compressed, const dev::RhsParams<double> &prm, cud
 
 } // namespace
 
-void DGX_FN(launch_rhs)(int D, int K, bool compressed, const dev::RhsParams<double> &prm,
+void DGX_FN(launch_rhs)(int D, int K, bool compressed, bool adv,
+                        const dev::RhsParams<double> &prm, cudaStream_t s)
+{
+  if (adv)
+    {
+      if (D == 2)
+        launch_rhs_d<2, true>(K, compressed, prm, s);
+      else
+        launch_rhs_d<3, true>(K, compressed, prm, s);
+      return;
+    }
+  if (D == 2)
+    launch_rhs_d<2, false>(K, compressed, prm, s);
+  else
+    launch_rhs_d<3, false>(K, compressed, prm, s);
+}
+
+void DGX_FN(launch_adv)(int D, int K, bool compressed, const dev::AdvParams<double> &prm,
                         cudaStream_t s)
 {
+#if DGX_BASIS == 2
+  (void)D, (void)K, (void)compressed, (void)prm, (void)s;
+  fail(Code::invalid_argument,
+       "advection: the Hermite-like basis is not implemented for advection on the device");
+#else
   if (D == 2)
-    launch_rhs_d<2>(K, compressed, prm, s);
+    launch_adv_d<2>(K, compressed, prm, s);
   else
-    launch_rhs_d<3>(K, compressed, prm, s);
+    launch_adv_d<3>(K, compressed, prm, s);
+#endif
 }
 
 void DGX_FN(upload_tables)(int K)

@@ -28,6 +28,22 @@ struct ApplyParams
   int n_owned; // slots >= n_owned are ghost cells (ghost-side tasks)
 };
 
+// Advection apply (OperatorKind::advection, operators.cpp:634-667 cell,
+// :942-960 interior faces, :1033-1060 boundary faces).
+template <typename Real>
+struct AdvParams
+{
+  const Real *u;
+  Real *y;
+  const Real *cell; // [geo][D][NQ] or compressed [geo][D]: J^{-1} c det(J) w (no w if compressed)
+  const Real *face; // [face][2][P] or compressed [face][2]: JxW_f (no w if compressed), c.n
+  const int *task_slot;
+  const int *task_geo;
+  const int2 *task_face;
+  int n_tasks;
+  int n_owned;
+};
+
 // Right-hand side assembly (assemble_rhs, operators.cpp:266-282): forcing
 // f at the owned cells' quadrature points times det(J) w_q, Dirichlet data g
 // at the computed faces' quadrature points (boundary faces only).
@@ -38,7 +54,7 @@ struct RhsParams
   const Real *detw; // [slot][q]
   const Real *g;    // [local face][qf] or null
   Real *y;
-  const Real *face_geo;
+  const Real *face_geo; // Laplacian face records, or the advection ones (AdvParams::face)
   const Real *penalty;
   const int *task_slot;
   const int2 *task_face;

@@ -15,7 +15,9 @@ namespace dgx
 namespace dev
 {
 
-template <typename Real, int D, int K, bool COMPRESSED, int BASIS>
+// ADV: the advection operator's boundary data term, (|c.n| - c.n) g JxW_f
+// (inflow only, operators.cpp:1053-1060), from the advection face records.
+template <typename Real, int D, int K, bool COMPRESSED, int BASIS, bool ADV>
 __global__ void __launch_bounds__(KernelShape<D, K>::THREADS)
   sipg_rhs_kernel(const RhsParams<Real> prm)
 {
@@ -68,28 +70,46 @@ __global__ void __launch_bounds__(KernelShape<D, K>::THREADS)
           if (tf.x == -1 && prm.g)
             {
               const int fid = tf.y & 0x3fffffff;
-              Real jxw, jo[D];
-              if constexpr (COMPRESSED)
+              if constexpr (ADV)
                 {
-                  const Real *fg = prm.face_geo + (long long)fid * (2 * D + 1);
-                  jxw = fg[0] * wf;
-#pragma unroll
-                  for (int b = 0; b < D; ++b)
-                    jo[b] = fg[1 + b];
+                  Real jxw, cn;
+                  if constexpr (COMPRESSED)
+                    {
+                      jxw = prm.face_geo[(long long)fid * 2] * wf;
+                      cn = prm.face_geo[(long long)fid * 2 + 1];
+                    }
+                  else
+                    {
+                      jxw = prm.face_geo[(long long)fid * 2 * P + p];
+                      cn = prm.face_geo[(long long)fid * 2 * P + P + p];
+                    }
+                  rv = (fabs(cn) - cn) * prm.g[(long long)fid * P + p] * jxw;
                 }
               else
                 {
-                  const Real *fg = prm.face_geo + (long long)fid * (2 * D + 1) * P + p;
-                  jxw = fg[0];
+                  Real jxw, jo[D];
+                  if constexpr (COMPRESSED)
+                    {
+                      const Real *fg = prm.face_geo + (long long)fid * (2 * D + 1);
+                      jxw = fg[0] * wf;
+#pragma unroll
+                      for (int b = 0; b < D; ++b)
+                        jo[b] = fg[1 + b];
+                    }
+                  else
+                    {
+                      const Real *fg = prm.face_geo + (long long)fid * (2 * D + 1) * P + p;
+                      jxw = fg[0];
+#pragma unroll
+                      for (int b = 0; b < D; ++b)
+                        jo[b] = fg[(1 + b) * P];
+                    }
+                  const Real gb = prm.g[(long long)fid * P + p] * jxw;
+                  rv = gb * prm.penalty[fid] * Real(2);
 #pragma unroll
                   for (int b = 0; b < D; ++b)
-                    jo[b] = fg[(1 + b) * P];
+                    gd[b] = -gb * jo[b];
                 }
-              const Real gb = prm.g[(long long)fid * P + p] * jxw;
-              rv = gb * prm.penalty[fid] * Real(2);
-#pragma unroll
-              for (int b = 0; b < D; ++b)
-                gd[b] = -gb * jo[b];
             }
           OUT[(2 * s) * FP + fp] = rv;
           OUT[(2 * s + 1) * FP + fp] = gd[A];

@@ -138,7 +138,9 @@ BASIS_KINDS = {"lagrange_gauss_lobatto": 0, "lagrange_gauss": 1, "hermite_like":
 @dataclass
 class OperatorConfig:
     """dg::OperatorConfig (operators.hpp:26-51) for this path. basis: one of
-    BASIS_KINDS (BasisKind, basis.hpp:10-15)."""
+    BASIS_KINDS (BasisKind, basis.hpp:10-15); kind: "laplacian" or
+    "advection" (with velocity = VelocityField::constant, or
+    variable_velocity=True and per-point values through set_velocity)."""
     d: int = 3
     p: int = 3
     W: int = 1
@@ -146,6 +148,8 @@ class OperatorConfig:
     basis: str = "lagrange_gauss_lobatto"
     geometry: str = "g3"
     precision: str = "fp64"
+    velocity: tuple = (1.0, 1.0, 1.0)
+    variable_velocity: bool = False
 
     def k(self):
         return self.p + 1
@@ -218,9 +222,8 @@ class RankOperator:
     def __init__(self, mesh: Mesh, partition: Partition, faces: np.ndarray,
                  geometry: Geometry, config: OperatorConfig, rank: int = 0,
                  device: int = 0):
-        if config.kind != "laplacian":
-            raise _lib.DgxInvalidArgument(
-                "RankOperator: this path implements the Laplacian only")
+        if config.kind not in ("laplacian", "advection"):
+            raise _lib.DgxInvalidArgument(f"RankOperator: unknown operator {config.kind!r}")
         if config.basis not in BASIS_KINDS:
             raise _lib.DgxInvalidArgument(f"RankOperator: unknown basis {config.basis!r}")
         self.mesh, self.config, self.rank = mesh, config, rank
@@ -241,6 +244,10 @@ class RankOperator:
         s.config.basis = BASIS_KINDS[config.basis]
         s.config.geometry_variant = 3 if config.geometry == "g3" else -1
         s.config.precision = {"fp64": 0, "fp32": 1}[config.precision]
+        s.config.kind = 1 if config.kind == "advection" else 0
+        for a in range(3):
+            s.config.velocity[a] = float(config.velocity[a]) if a < len(config.velocity) else 0.0
+        s.config.variable_velocity = int(bool(config.variable_velocity))
         g = s.geometry
         g.source = _SOURCES[geometry.source]
         g.coefficient = 1 if geometry.coefficient else 0
@@ -258,8 +265,9 @@ class RankOperator:
             keep.append(a)
             g.compressed = int(bool(geometry.arrays.get("compressed", False)))
             for name in ("inv_jac_t", "jxw", "face_jxw", "face_jni", "face_jne",
-                         "penalty"):
-                setattr(g, name, a[name].ctypes.data)
+                         "penalty", "face_normal"):
+                if name in a:
+                    setattr(g, name, a[name].ctypes.data)
         h = C.c_void_p()
         check(lib().dgx_create(C.byref(s), C.c_int(device), C.byref(h)))
         self._h = h
@@ -326,6 +334,11 @@ class RankOperator:
         if w == 1:
             return out.reshape(-1, lay.dofs_per_cell // (self.config.p + 1), d)
         return out.astype(bool)
+
+    def set_velocity(self, c_cells, c_faces, stream=None):
+        """Advection with a variable velocity: c at quadrature_points("cells")
+        and quadrature_points("faces") (CUDA tensors, [..., d] flattened)."""
+        check(lib().dgx_set_velocity(self._h, _ptr(c_cells), _ptr(c_faces), _stream(stream)))
 
     def assemble_rhs(self, rhs, forcing=None, dirichlet=None, stream=None):
         """RankOperator::assemble_rhs (operators.cpp:266-282). forcing /

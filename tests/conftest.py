@@ -44,6 +44,10 @@ class Case:
         # BasisKind: 0 lagrange_gauss_lobatto, 1 lagrange_gauss, 2 hermite_like
         self.basis = int(self.g.get("basis", 0))
         self.basis_name = ("lagrange_gauss_lobatto", "lagrange_gauss", "hermite_like")[self.basis]
+        adv = self.g.get("advection")
+        self.kind = "advection" if adv is not None else "laplacian"
+        self.velocity = tuple(float(v) for v in adv[:3]) if adv is not None else (1.0, 1.0, 1.0)
+        self.velocity_field = int(adv[3]) if adv is not None else 0
         self.seeds = sorted(int(k[1:]) for k in self.g if k.startswith("x") and k[1:].isdigit())
 
     @property

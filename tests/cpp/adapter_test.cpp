@@ -63,16 +63,23 @@ static std::vector<double> distributed_apply(std::vector<std::unique_ptr<Op>> &o
   return out;
 }
 
-static int run_case(int d, int cells, int p, double amp, bool periodic, int m, int nr)
+// op: 0 Laplacian with the Gauss-Lobatto basis (BASELINE), 1 the reference
+// default configuration (Hermite-like basis for p >= 3), 2 advection
+static int run_case(int d, int cells, int p, double amp, bool periodic, int m, int nr, int op = 0)
 {
   const Mesh mesh = make_box_mesh(d, cells, amp, periodic, m);
-  OperatorConfig cfg = make_operator_config(OperatorKind::laplacian, d, p, 1, GeometryVariant::g3);
-  cfg.basis = BasisKind::lagrange_gauss_lobatto;
+  OperatorConfig cfg = make_operator_config(op == 2 ? OperatorKind::advection : OperatorKind::laplacian,
+                                            d, p, 1, GeometryVariant::g3);
+  if (op == 0)
+    cfg.basis = BasisKind::lagrange_gauss_lobatto;
+  if (op == 2)
+    cfg.velocity.constant = {0.85, -0.6, 0.35};
   const auto faces = enumerate_faces(mesh);
   Partition part = partition_cells(mesh, nr);
   assign_face_owners(mesh, faces, part);
   auto geom = std::make_shared<GeometryCache>(
-    precompute_geometry(mesh, faces, cfg.k(), cfg.k(), cfg.geometry, cfg.equation()));
+    precompute_geometry(mesh, faces, cfg.k(), cfg.k(), cfg.geometry, cfg.equation(),
+                        cfg.velocity));
   std::vector<std::unique_ptr<RankOperator>> ref;
   std::vector<std::unique_ptr<dgx_ref::RankOperator>> gpu;
   for (int r = 0; r < nr; ++r)
@@ -86,8 +93,8 @@ static int run_case(int d, int cells, int p, double amp, bool periodic, int m, i
   const auto y_gpu = distributed_apply(gpu, faces, part, cfg, x);
   const double err = rel_linf(y_gpu, y_ref);
   const bool ok = err < 1e-12;
-  std::printf("%s d=%d cells=%d p=%d amp=%.2f periodic=%d m=%d ranks=%d rel_linf=%.2e\n",
-              ok ? "PASS" : "FAIL", d, cells, p, amp, periodic, m, nr, err);
+  std::printf("%s op=%d d=%d cells=%d p=%d amp=%.2f periodic=%d m=%d ranks=%d rel_linf=%.2e\n",
+              ok ? "PASS" : "FAIL", op, d, cells, p, amp, periodic, m, nr, err);
   // a ghosted layout without hooks is a logic error (operators.cpp:238-240)
   if (nr > 1)
     {
@@ -118,6 +125,10 @@ int main()
   fails += run_case(2, 4, 2, 0.05, true, 2, 2);
   fails += run_case(2, 5, 5, 0.04, false, 2, 4);
   fails += run_case(3, 3, 3, 0.06, false, 3, 3);
+  fails += run_case(3, 3, 5, 0.05, false, 2, 3, 1); // reference default: Hermite-like
+  fails += run_case(2, 5, 4, 0.04, true, 2, 2, 1);
+  fails += run_case(3, 3, 3, 0.05, false, 2, 3, 2); // advection
+  fails += run_case(2, 6, 5, 0.0, true, 1, 2, 2);
   std::printf("%s\n", fails ? "FAILED" : "ALL PASS");
   return fails ? 1 : 0;
 }

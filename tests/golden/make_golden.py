@@ -17,7 +17,7 @@ Cases follow BASELINE.json's configs at parity-test sizes:
     precompute_geometry on reference meshes) and injected into the
     reference RankOperator.
 
-usage: python tests/golden/make_golden.py [--other-bases]
+usage: python tests/golden/make_golden.py [--other-bases | --advection]
 """
 import os
 import sys
@@ -50,8 +50,9 @@ def world_arrays(w, n_ranks, prefix="", basis="gl"):
                 [p["neighbor"] for p in pl], np.int32)
             for i, p in enumerate(pl):
                 out[f"{prefix}r{r}_{which}{i}_cells"] = p["cells"]
-                if basis != "gl":
-                    # Hermite: two layers per coupled face (ghost_exchange.cpp:49-96)
+                if basis != "gl" or getattr(w, "kind", "laplacian") == "advection":
+                    # Hermite: two layers per coupled face, nodal values: one
+                    # (ghost_exchange.cpp:46-96)
                     out[f"{prefix}r{r}_{which}{i}_offsets"] = p["offsets"]
                     out[f"{prefix}r{r}_{which}{i}_dofs"] = p["dofs"]
                     continue
@@ -72,13 +73,17 @@ BASIS_ID = {"gl": 0, "gauss": 1, "hermite": 2}
 
 
 def reference_case(name, d, cells, p, periodic, amplitude, m, n_ranks, seeds,
-                   dense=False, geometry=True, basis="gl"):
+                   dense=False, geometry=True, basis="gl", kind="laplacian",
+                   velocity=(1.0, 1.0, 1.0), velocity_field=0):
     w = R.World(d, cells, p, n_ranks=n_ranks, amplitude=amplitude,
-                mapping_degree=m, periodic=periodic, basis=basis)
+                mapping_degree=m, periodic=periodic, basis=basis, kind=kind,
+                velocity=velocity, velocity_field=velocity_field)
     arr = dict(meta=np.array([d, *cells, p, int(periodic), m, n_ranks], np.int64),
                amplitude=np.array(amplitude))
     if basis != "gl":
         arr["basis"] = np.array(BASIS_ID[basis])
+    if kind == "advection":
+        arr["advection"] = np.array([*velocity, velocity_field], np.float64)
     for s in seeds:
         x = R.random_vector(w.n_dofs, s)
         arr[f"x{s}"] = x
@@ -163,7 +168,30 @@ def other_bases():
     reference_case("gauss2d_p2_periodic", 2, [4, 4], 2, True, 0.0, 1, 1, [29], basis="gauss")
 
 
+def advection():
+    """The advection operator (OperatorKind::advection), the paper's other
+    operator: constant and variable transport fields, one-layer plans."""
+    c = (0.85, 0.6, 0.35)
+    reference_case("adv3d_p3_m2", 3, [3, 3, 3], 3, False, 0.05, 2, 1, [31], kind="advection",
+                   velocity=c)
+    reference_case("adv3d_p4_m2_r3", 3, [3, 3, 4], 4, False, 0.05, 2, 3, [32],
+                   kind="advection", velocity=c)
+    reference_case("adv2d_periodic_p5_m3_r2", 2, [5, 4], 5, True, 0.06, 3, 2, [33],
+                   kind="advection", velocity=(-0.4, 0.9, 0.0))
+    reference_case("adv3d_cart_p6_r2", 3, [3, 3, 3], 6, False, 0.0, 1, 2, [34],
+                   kind="advection", velocity=c)
+    reference_case("adv2d_field_p3_m2_r2", 2, [4, 4], 3, False, 0.05, 2, 2, [35],
+                   kind="advection", velocity_field=1)
+    reference_case("adv3d_field_p2_m2", 3, [3, 2, 3], 2, False, 0.04, 2, 1, [36],
+                   kind="advection", velocity_field=1)
+    reference_case("adv_gauss3d_p3_m2_r2", 3, [3, 2, 2], 3, False, 0.05, 2, 2, [37],
+                   kind="advection", velocity=c, basis="gauss")
+
+
 def main():
+    if "--advection" in sys.argv:
+        advection()
+        return
     if "--other-bases" in sys.argv:
         other_bases()
         return
@@ -192,5 +220,6 @@ def main():
 
 if __name__ == "__main__":
     main()
-    if "--other-bases" not in sys.argv:
+    if "--other-bases" not in sys.argv and "--advection" not in sys.argv:
         other_bases()
+        advection()

@@ -53,8 +53,23 @@ def build(c: Case, rank=0, n_ranks=None, precision="fp64", p=None):
     faces = D.enumerate_faces(mesh)
     part = D.partition_cells(mesh, n_ranks or c.n_ranks)
     D.assign_face_owners(mesh, faces, part)
-    cfg = D.OperatorConfig(d=c.d, p=p or c.p, precision=precision, basis=c.basis_name)
-    return D.RankOperator(mesh, part, faces, geometry_of(c), cfg, rank), part
+    cfg = D.OperatorConfig(d=c.d, p=p or c.p, precision=precision, basis=c.basis_name,
+                           kind=c.kind, velocity=c.velocity,
+                           variable_velocity=bool(c.velocity_field))
+    op = D.RankOperator(mesh, part, faces, geometry_of(c), cfg, rank)
+    if c.velocity_field:
+        set_field_velocity(op, c.d)
+    return op, part
+
+
+def set_field_velocity(op, d):
+    """The harness's variable transport field at the device quadrature points."""
+    import torch as t
+    from oracle import reflib as R
+    cc = t.tensor(R.test_velocity(d, op.quadrature_points("cells")).ravel(), device="cuda")
+    cf = t.tensor(R.test_velocity(d, op.quadrature_points("faces")).ravel(), device="cuda")
+    op.set_velocity(cc, cf)
+    t.cuda.synchronize()
 
 
 def apply_single(torch, op, x, dtype=None):
@@ -120,8 +135,21 @@ def test_golden_rank_partitioned(torch, name):
     nq = (c.p + 1) ** c.d
     x = c.g[f"x{c.seeds[0]}"]
     y, local = apply_serial_ranks(torch, ops, parts, x, nq, return_local=True,
-                                  planned_only=c.basis == 2)
+                                  planned_only=c.basis == 2 or c.kind == "advection")
     assert rel_linf(y, c.g[f"y{c.seeds[0]}"]) < TOL64
+    if c.kind == "advection":
+        from oracle import reflib as R
+        if not R.available():
+            return
+        w = R.World(c.d, c.cells, c.p, n_ranks=c.n_ranks, amplitude=c.amplitude,
+                    mapping_degree=c.m, periodic=c.periodic,
+                    basis={0: "gl", 1: "gauss", 2: "hermite"}[c.basis], kind="advection",
+                    velocity=c.velocity, velocity_field=c.velocity_field)
+        for r, (u_loc, y_loc) in enumerate(local):
+            assert np.all(np.isfinite(y_loc))
+            ref = w.apply_rank_local(r, np.nan_to_num(u_loc, nan=0.0))
+            assert rel_linf(y_loc, ref) < TOL64
+        return
     # per-rank state before compress (ghost slots hold remote contributions)
     P = O.Problem(c.d, c.cells, c.p, periodic=c.periodic, deform=c.deform(),
                   coefficient=c.coefficient, n_ranks=c.n_ranks, basis=c.basis)
@@ -533,3 +561,87 @@ def test_convergence_study(torch, d, p):
         errs.append(_l2_error(op, x.cpu().numpy(), cfg.basis, p, d))
     rates = [np.log2(errs[i] / errs[i + 1]) for i in range(len(errs) - 1)]
     assert rates[-1] > p + 0.5, (errs, rates)
+
+
+ADV_RANDOM = [
+    # d, cells, p, periodic, amplitude, m, ranks, velocity, field, basis
+    (3, [3, 3, 2], 1, False, 0.05, 2, 1, (0.85, 0.6, 0.35), 0, "gl"),
+    (3, [3, 2, 3], 2, True, 0.04, 2, 2, (-0.3, 0.8, 0.5), 0, "gl"),
+    (3, [2, 3, 3], 5, False, 0.05, 2, 3, (0.85, 0.6, 0.35), 0, "gl"),
+    (3, [2, 2, 2], 8, False, 0.05, 3, 1, (0.2, -0.7, 0.9), 0, "gl"),
+    (2, [6, 5], 7, False, 0.06, 2, 2, (0.85, 0.6, 0.0), 0, "gl"),
+    (2, [5, 5], 10, True, 0.03, 2, 1, (0.5, -0.5, 0.0), 0, "gl"),
+    (3, [3, 3, 3], 4, False, 0.0, 1, 2, (0.85, 0.6, 0.35), 0, "gl"),
+    (3, [3, 3, 2], 3, False, 0.05, 2, 2, (0.0, 0.0, 0.0), 1, "gl"),
+    (2, [4, 4], 6, False, 0.05, 2, 1, (0.0, 0.0, 0.0), 1, "gauss"),
+]
+
+
+@pytest.mark.parametrize("cfg", ADV_RANDOM, ids=lambda c: f"d{c[0]}p{c[2]}r{c[6]}f{c[8]}-{c[9]}")
+def test_advection_against_reference(torch, cfg):
+    """The advection apply (OperatorKind::advection, operators.cpp:634-667,
+    942-960, 1033-1060) against the reference RankOperator on the same
+    inputs; multi-rank cases ship only the planned one-layer ghost values."""
+    from oracle import reflib as R
+    if not R.available():
+        pytest.skip("reference library not built")
+    D = dgx()
+    d, cells, p, periodic, amp, m, nr, vel, field, basis = cfg
+    w = R.World(d, cells, p, n_ranks=nr, amplitude=amp, mapping_degree=m, periodic=periodic,
+                basis=basis, kind="advection", velocity=vel, velocity_field=field)
+    x = R.random_vector(w.n_dofs, 2000 + p)
+    y_ref = w.apply(x)
+    mesh = D.make_box_mesh(d, cells, amp, periodic, m)
+    faces = D.enumerate_faces(mesh)
+    part = D.partition_cells(mesh, nr)
+    D.assign_face_owners(mesh, faces, part)
+    cfg_ = D.OperatorConfig(d=d, p=p, kind="advection", velocity=vel,
+                            variable_velocity=bool(field),
+                            basis={"gl": "lagrange_gauss_lobatto", "gauss": "lagrange_gauss"}[basis])
+    ops = []
+    for r in range(nr):
+        op = D.RankOperator(mesh, part, faces, D.Geometry(source="mesh"), cfg_, r)
+        if field:
+            set_field_velocity(op, d)
+        ops.append(op)
+    if nr == 1:
+        y = apply_single(torch, ops[0], x)
+    else:
+        y = apply_serial_ranks(torch, ops, None, x, (p + 1) ** d, planned_only=basis == "gl")
+    assert rel_linf(y, y_ref) < TOL64 and rel_l2(y, y_ref) < TOL64, (rel_linf(y, y_ref),)
+
+
+@pytest.mark.parametrize("field", [0, 1])
+def test_advection_rhs_against_reference(torch, field):
+    """assemble_rhs of the advection operator: forcing c.grad u and the inflow
+    data (|c.n| - c.n) g (operators.cpp:1053-1060)."""
+    from oracle import reflib as R
+    if not R.available():
+        pytest.skip("reference library not built")
+    D = dgx()
+    d, cells, p, vel = 3, [3, 3, 3], 3, (0.85, 0.6, 0.35)
+    w = R.World(d, cells, p, n_ranks=2, amplitude=0.05, mapping_degree=2, kind="advection",
+                velocity=vel, velocity_field=field, manufactured=True)
+    mesh = D.make_box_mesh(d, cells, 0.05, False, 2)
+    faces = D.enumerate_faces(mesh)
+    part = D.partition_cells(mesh, 2)
+    D.assign_face_owners(mesh, faces, part)
+    for r in range(2):
+        op = D.RankOperator(mesh, part, faces, D.Geometry(source="mesh"),
+                            D.OperatorConfig(d=d, p=p, kind="advection", velocity=vel,
+                                             variable_velocity=bool(field)), r)
+        xq, xf = op.quadrature_points("cells"), op.quadrature_points("faces")
+        if field:
+            set_field_velocity(op, d)
+            cq = R.test_velocity(d, xq)
+        else:
+            cq = np.broadcast_to(np.array(vel[:d]), xq.shape)
+        fq = np.sum(cq * R.manufactured_gradient(d, xq), axis=-1)
+        f = torch.tensor(fq.ravel(), device="cuda")
+        g = torch.tensor(R.manufactured_solution(d, xf).ravel(), device="cuda")
+        rhs = torch.empty(op.layout().total_size, dtype=torch.float64, device="cuda")
+        op.assemble_rhs(rhs, f, g)
+        torch.cuda.synchronize()
+        ref = w.rhs(r)
+        got = rhs.cpu().numpy()
+        assert rel_linf(got, ref) < TOL64, rel_linf(got, ref)

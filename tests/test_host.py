@@ -60,7 +60,8 @@ def host_op(c: Case, rank, n_ranks=None, p=None):
     faces = dgx.enumerate_faces(mesh)
     part = dgx.partition_cells(mesh, n_ranks or c.n_ranks)
     dgx.assign_face_owners(mesh, faces, part)
-    cfg = dgx.OperatorConfig(d=c.d, p=p or c.p, basis=c.basis_name)
+    cfg = dgx.OperatorConfig(d=c.d, p=p or c.p, basis=c.basis_name, kind=c.kind,
+                             velocity=c.velocity, variable_velocity=bool(c.velocity_field))
     return dgx.RankOperator(mesh, part, faces, dgx.Geometry(), cfg, rank, device=-1), faces, part
 
 
