@@ -55,6 +55,11 @@ CONFIGS = {
     "c5h": (3, 160, 6, False, "cart", False, "fp64", 4,
             "C5h: 3D SIPG, Cartesian 160^3, p=6, affine, Hermite-like basis, fp64"),
 }
+# the paper's other operator on the C4 workload size (reference mesh
+# deformation, amplitude 0.05, mapping degree 2; constant transport field)
+CONFIGS["a4"] = (3, 128, 5, False, "mesh", False, "fp64", 3,
+                 "A4: 3D advection, deformed 128^3 (reference mapping m=2), p=5, c=(0.85,0.6,0.35), fp64")
+ADVECTION = {"a4": (0.85, 0.6, 0.35)}
 # BasisKind per config (default: the nodal Gauss-Lobatto basis BASELINE names)
 BASIS = {"c4h": "hermite_like", "c3h": "hermite_like", "c5h": "hermite_like"}
 # reference instrumented flop count per DoF (counters x W / applies,
@@ -62,7 +67,7 @@ BASIS = {"c4h": "hermite_like", "c3h": "hermite_like", "c5h": "hermite_like"}
 REF_FLOPS_PER_DOF = {"c4": 240.0, "c3": 215.52, "c5": 260.82, "c5f32": 260.82,
                      "c1": 198.0, "c2": 105.80,
                      # Hermite-like: plain (not even-odd) S passes, same counters
-                     "c4h": 268.0, "c3h": 242.4, "c5h": 293.14}
+                     "c4h": 268.0, "c3h": 242.4, "c5h": 293.14, "a4": 93.0}
 
 
 def peaks():
@@ -172,8 +177,13 @@ class RefBench:
             geo["compressed"] = False
         best = None
         for W in (4, 8):
+            adv = ADVECTION.get(cfg_name)
             w = R.World(d, cells, p, n_ranks=self.n_ranks, periodic=periodic, W=W, geometry=geo,
-                        basis=BASIS.get(cfg_name, "lagrange_gauss_lobatto"))
+                        basis=BASIS.get(cfg_name, "lagrange_gauss_lobatto"),
+                        amplitude=0.05 if kind == "mesh" else 0.0,
+                        mapping_degree=2 if kind == "mesh" else 1,
+                        kind="advection" if adv else "laplacian",
+                        velocity=adv or (1.0, 1.0, 1.0))
             w.time(1)
             t = min(w.time(1) for _ in range(3))
             if best is None or t < best[0]:
@@ -216,7 +226,8 @@ def main():
     if args.cells:
         n = args.cells
     n_dofs = n ** d * (p + 1) ** d
-    metric = "DG Laplacian apply throughput (DoFs/s)"
+    metric = ("DG advection apply throughput (DoFs/s)" if ADVECTION.get(args.config)
+              else "DG Laplacian apply throughput (DoFs/s)")
     config = {"workload": label, "cells": [n] * d, "degree": p, "n_dofs": n_dofs,
               "basis": BASIS.get(args.config, "lagrange_gauss_lobatto"),
               "seed": seed, "partition": f"contiguous lexicographic slabs x{args.gpus}",
@@ -252,15 +263,18 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
     t_setup = time.time()
-    mesh = dgx.make_box_mesh(d, n, 0.0, periodic, 1)
+    mesh = (dgx.make_box_mesh(d, n, 0.05, periodic, 2) if kind == "mesh"
+            else dgx.make_box_mesh(d, n, 0.0, periodic, 1))
     faces = dgx.enumerate_faces(mesh)
     part = dgx.partition_cells(mesh, ws)
     dgx.assign_face_owners(mesh, faces, part)
     geo = (dgx.Geometry(source="vertex_bump", vertex_bump_eps=0.1, coefficient="a1" if coef else None)
            if kind == "vertex" else dgx.Geometry(source="mesh"))
-    op = dgx.RankOperator(mesh, part, faces, geo, dgx.OperatorConfig(d=d, p=p, precision=prec,
-                                         basis=BASIS.get(args.config, "lagrange_gauss_lobatto")),
-                          rank, device=local)
+    adv = ADVECTION.get(args.config)
+    op = dgx.RankOperator(mesh, part, faces, geo, dgx.OperatorConfig(
+        d=d, p=p, precision=prec, basis=BASIS.get(args.config, "lagrange_gauss_lobatto"),
+        kind="advection" if adv else "laplacian", velocity=adv or (1.0, 1.0, 1.0)),
+        rank, device=local)
     lay = op.layout()
     hooks = None
     if ws > 1:

@@ -746,8 +746,9 @@ dgx_stats Operator::stats() const
   st.kernel_launches_per_apply = (n_inner_ > 0) + (n_coupled_ > 0);
   const double es = precision_ == 1 ? 4.0 : 8.0;
   st.bytes_vectors = 2.0 * es * (double)layout_.owned_size();
-  st.bytes_cell_geometry = es * (double)cell_geo_.size();
-  st.bytes_face_geometry = es * (double)(face_geo_.size() + penalty_.size());
+  st.bytes_cell_geometry = es * (double)(kind_ == 1 ? adv_cell_.size() : cell_geo_.size());
+  st.bytes_face_geometry =
+    es * (double)(kind_ == 1 ? adv_face_.size() : face_geo_.size() + penalty_.size());
   st.cells_per_cta = kernel_cells_per_cta(d_, k_);
   long long P = nq_ / k_;
   st.threads_per_cta = static_cast<int>(st.cells_per_cta * P);
