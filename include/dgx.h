@@ -107,6 +107,7 @@ typedef struct dgx_geometry
   const double *face_jxw, *face_jni, *face_jne, *penalty; /* HOST_ARRAYS */
   const double *face_normal; /* HOST_ARRAYS, advection: GeometryCache::face_normal
                                 [face][qf][d] */
+  const double *coeff;       /* HOST_ARRAYS, g4: GeometryCache::coeff [cell][q][d(d+1)/2] */
 } dgx_geometry;
 
 /* Replaces dg::OperatorConfig (operators.hpp:26-51) for this path: the
@@ -120,7 +121,9 @@ typedef struct dgx_config
                            1 lagrange_gauss, 2 hermite_like (p >= 3; the
                            reference default for the Laplacian at p >= 3,
                            make_operator_config, operators.cpp:27-41) */
-  int geometry_variant; /* 3: g3 (others rejected) */
+  int geometry_variant; /* 3: g3 (J^{-T} and JxW per point), 4: g4 (the merged
+                           coefficient J^{-1}J^{-T} det(J) w, geometry.cpp:219-246,
+                           370-388); others rejected */
   int precision;        /* 0: fp64, 1: fp32 */
   int kind;             /* OperatorKind: 0 laplacian, 1 advection (fp64, nodal or
                            Lagrange-Gauss basis) */

@@ -43,6 +43,7 @@ thread_local std::string g_err;
 thread_local int g_basis = 0; // BasisKind for new worlds; -1 = reference default
 thread_local int g_manufactured = 0; // forcing/dirichlet of the convergence study
 thread_local int g_kind = 0;          // 0 laplacian, 1 advection
+thread_local int g_variant = 3;       // geometry variant of new worlds: 3 g3, 4 g4
 thread_local double g_velocity[3] = {1, 1, 1};
 thread_local int g_velocity_field = 0; // 1: the variable test field below
 
@@ -144,7 +145,8 @@ World *make_world_common(int d, const int *cells, double amplitude,
                        {0, 0, 0}, {1, 1, 1}, amplitude, mapping_degree,
                        boundary);
   const OperatorKind kind = g_kind == 1 ? OperatorKind::advection : OperatorKind::laplacian;
-  w->cfg = make_operator_config(kind, d, p, W, GeometryVariant::g3);
+  w->cfg = make_operator_config(kind, d, p, W,
+                                g_variant == 4 ? GeometryVariant::g4 : GeometryVariant::g3);
   if (g_basis >= 0)
     w->cfg.basis = static_cast<BasisKind>(g_basis); // GL unless selected
   if (kind == OperatorKind::advection)
@@ -227,6 +229,18 @@ int dgref_set_operator(int kind, const double *c, int field)
       for (int a = 0; a < 3; ++a)
         g_velocity[a] = c[a];
     g_velocity_field = field;
+  });
+}
+
+// Geometry variant of the worlds created next (3: g3, 4: g4; the reference's
+// precompute_geometry stores the merged coefficient for g4,
+// geometry.cpp:370-388).
+int dgref_set_variant(int variant)
+{
+  return guard([&] {
+    if (variant != 3 && variant != 4)
+      throw std::invalid_argument("dgref_set_variant: g3 or g4");
+    g_variant = variant;
   });
 }
 
@@ -408,6 +422,7 @@ int dgref_world_geometry(void *wp, int which, double *out, long long *n)
       case 8: v = &g.face_qpoints; break;
       case 9: v = &g.wq_cell; break;
       case 10: v = &g.wq_face; break;
+      case 11: v = &g.coeff; break;
       default: throw std::invalid_argument("dgref_world_geometry: bad array");
       }
     if (out)

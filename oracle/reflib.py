@@ -126,7 +126,7 @@ def _shape_matrices(p: int):
 
 GEOM_NAMES = ["inv_jac_t", "jxw", "face_jxw", "face_jni", "face_jne",
               "penalty", "cell_volume", "face_normal", "face_qpoints",
-              "wq_cell", "wq_face"]
+              "wq_cell", "wq_face", "coeff"]
 
 
 class World:
@@ -136,7 +136,7 @@ class World:
     def __init__(self, d, cells, p, n_ranks=1, amplitude=0.0,
                  mapping_degree=1, periodic=False, W=1, geometry=None, basis="gl",
                  manufactured=False, kind="laplacian", velocity=(1.0, 1.0, 1.0),
-                 velocity_field=0):
+                 velocity_field=0, variant="g3"):
         """manufactured: forcing / Dirichlet data of the reference convergence
         study (bench.cpp:437-560) for rhs(). kind "advection": the transport
         operator with a constant velocity, or velocity_field=1 (the harness's
@@ -146,6 +146,7 @@ class World:
         _chk(lib().dgref_set_operator(C.c_int(1 if kind == "advection" else 0), vel,
                                       C.c_int(velocity_field)))
         self.kind = kind
+        _chk(lib().dgref_set_variant(C.c_int(4 if variant == "g4" else 3)))
         try:
             with _basis(basis):
                 self._create(d, cells, p, n_ranks, amplitude, mapping_degree, periodic, W,
@@ -153,6 +154,7 @@ class World:
         finally:
             lib().dgref_set_manufactured(C.c_int(0))
             lib().dgref_set_operator(C.c_int(0), None, C.c_int(0))
+            lib().dgref_set_variant(C.c_int(3))
 
     def _create(self, d, cells, p, n_ranks, amplitude, mapping_degree, periodic, W,
                 geometry):

@@ -60,7 +60,7 @@ class CGeometry(C.Structure):
                 ("inv_jac_t", C.c_void_p), ("jxw", C.c_void_p),
                 ("face_jxw", C.c_void_p), ("face_jni", C.c_void_p),
                 ("face_jne", C.c_void_p), ("penalty", C.c_void_p),
-                ("face_normal", C.c_void_p)]
+                ("face_normal", C.c_void_p), ("coeff", C.c_void_p)]
 
 
 class CConfig(C.Structure):

@@ -120,6 +120,7 @@ struct GeometryJob
   int d = 3, k = 2, m = 1;
   bool compress = false;
   int coefficient = 0;  // 1: a(x) = 1 + 0.5 sin(pi x) cos(pi y) folded in
+  bool g4 = false;      // cell records: merged symmetric coefficient (variant g4)
   double cart_volume = 0; // > 0: Cartesian mesh, every cell has this volume
   const double *support = nullptr; // device [n_slots][(m+1)^d][d]
   int n_slots = 0;       // local cells with support points

@@ -170,6 +170,24 @@ __global__ void cell_geometry_kernel(GeometryJob job, GeoConst gc, int *bad)
   double det_jxw = job.compress ? det : det * cell_weight(gc, d, k, rec);
   if (job.coefficient)
     det_jxw *= coef_a(x);
+  if (job.g4)
+    {
+      // symmetric_coefficient (geometry.cpp:219-246): (J^{-1} J^{-T})_ij
+      // det(J) w, entries (00, 11, 22, 01, 02, 12) / (00, 11, 01)
+      const int ns = d * (d + 1) / 2;
+      const int ii[6] = {0, 1, d == 3 ? 2 : 0, 0, 0, 1};
+      const int jj[6] = {0, 1, d == 3 ? 2 : 1, 1, 2, 2};
+      double *out = job.cell_geo + (long long)c * ns * nrec + rec;
+      for (int e = 0; e < ns; ++e)
+        {
+          const int i = d == 3 ? ii[e] : (e < 2 ? e : 0), j = d == 3 ? jj[e] : (e < 2 ? e : 1);
+          double sum = 0;
+          for (int a = 0; a < d; ++a)
+            sum += jit[a * d + i] * jit[a * d + j];
+          out[e * nrec] = sum * det_jxw;
+        }
+      return;
+    }
   const int nc = d * d + 1;
   double *out = job.cell_geo + (long long)c * nc * nrec + rec;
   for (int i = 0; i < d * d; ++i)

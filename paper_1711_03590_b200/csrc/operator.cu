@@ -35,8 +35,12 @@ MeshDesc to_mesh(const dgx_mesh &m)
 Operator::Operator(const dgx_setup &s, int device) : device_(device)
 {
   const dgx_config &c = s.config;
-  if (c.geometry_variant != 3)
-    fail(Code::invalid_argument, "RankOperator: only geometry variant g3 is implemented");
+  if (c.geometry_variant != 3 && c.geometry_variant != 4)
+    fail(Code::invalid_argument,
+         "RankOperator: geometry variants g3 and g4 are implemented on the device");
+  sym_ = c.geometry_variant == 4;
+  if (sym_ && c.kind == 1)
+    fail(Code::invalid_argument, "RankOperator: advection runs with geometry variant g3");
   if (c.d != s.mesh.d)
     fail(Code::invalid_argument, "RankOperator: mesh dimension mismatch");
   if (c.W != 1 && c.W != 2 && c.W != 4 && c.W != 8)
@@ -288,7 +292,8 @@ void Operator::build_geometry(const dgx_setup &s, const std::vector<RawFace> &fa
   const long long n_owned = layout_.n_owned;
   const long long n_slots = n_owned + (long long)layout_.ghosts.size();
   const long long nmy = (long long)layout_.my_faces.size();
-  const int ncomp = d_ * d_ + 1;
+  // g3: J^{-T} (d^2) and JxW; g4: the d(d+1)/2 merged coefficients
+  const int ncomp = sym_ ? d_ * (d_ + 1) / 2 : d_ * d_ + 1;
   std::vector<std::uint32_t> slot_cells(n_slots);
   for (long long i = 0; i < n_owned; ++i)
     slot_cells[i] = layout_.owned_begin + (std::uint32_t)i;
@@ -299,7 +304,8 @@ void Operator::build_geometry(const dgx_setup &s, const std::vector<RawFace> &fa
     {
       if (g.coefficient)
         fail(Code::invalid_argument, "geometry: fold the coefficient into the host arrays");
-      if (!g.inv_jac_t || !g.jxw || !g.face_jxw || !g.face_jni || !g.face_jne || !g.penalty)
+      if ((sym_ ? !g.coeff : (!g.inv_jac_t || !g.jxw)) || !g.face_jxw || !g.face_jni ||
+          !g.face_jne || !g.penalty)
         fail(Code::invalid_argument, "geometry: missing host arrays");
       compressed_ = g.compressed != 0;
       const long long nrec = compressed_ ? 1 : nq_;
@@ -309,6 +315,13 @@ void Operator::build_geometry(const dgx_setup &s, const std::vector<RawFace> &fa
           const long long gc = layout_.owned_begin + c;
           for (long long r = 0; r < nrec; ++r)
             {
+              if (sym_)
+                {
+                  // GeometryCache::coeff [cell][q][d(d+1)/2]
+                  for (int i = 0; i < ncomp; ++i)
+                    cg[(c * ncomp + i) * nrec + r] = g.coeff[(gc * nrec + r) * ncomp + i];
+                  continue;
+                }
               const double *jit = g.inv_jac_t + (gc * nrec + r) * d_ * d_;
               for (int i = 0; i < d_ * d_; ++i)
                 cg[(c * ncomp + i) * nrec + r] = jit[i];
@@ -459,6 +472,7 @@ void Operator::build_geometry(const dgx_setup &s, const std::vector<RawFace> &fa
       job.m = m;
       job.compress = compressed_;
       job.coefficient = g.coefficient;
+      job.g4 = sym_;
       if (cartesian)
         {
           double v = 1.0;
@@ -561,6 +575,7 @@ void Operator::launch_range(int begin, int count, const Real *u, Real *y, cudaSt
   prm.task_face = task_face_.get() + (long long)begin * 2 * d_;
   prm.n_tasks = count;
   prm.n_owned = static_cast<int>(layout_.n_owned);
+  prm.sym = sym_ ? 1 : 0;
   launch_apply<Real>(d_, k_, basis_, compressed_, prm, s);
 }
 
@@ -669,6 +684,9 @@ void Operator::ensure_detw()
     }
   // host-array geometry (the reference's GeometryCache, no coefficient):
   // JxW is det(J) w_q, or det(J) for a compressed record
+  if (sym_)
+    fail(Code::invalid_argument,
+         "assemble_rhs: a g4 host-array cache carries no JxW for the forcing");
   const std::vector<double> cg = cell_geo_.download();
   const int ncomp = d_ * d_ + 1;
   const Quad1D qg = gauss(k_);

@@ -70,6 +70,7 @@ private:
   MeshDesc mesh_;
   int d_ = 3, p_ = 1, k_ = 2, precision_ = 0, device_ = 0, n_ranks_ = 1, basis_ = 0;
   int kind_ = 0; // 0 Laplacian, 1 advection
+  bool sym_ = false; // geometry variant g4 (merged symmetric coefficient)
   double velocity_[3] = {1, 1, 1};
   bool variable_velocity_ = false;
   DeviceArray<double> normals_;           // advection: [face][d][qf or 1]

@@ -592,7 +592,60 @@ __global__ void __launch_bounds__(KernelShape<D, K>::THREADS, KernelShape<D, K>:
       {
         const int q = pidx<D, K, D - 1>(p, m);
         Real t[D];
-        if (geo >= 0)
+        if (geo >= 0 && prm.sym)
+          {
+            // g4: t = C g with the merged symmetric coefficient
+            // (laplacian_coefficient, operators.cpp:712-733)
+            constexpr int NS = D * (D + 1) / 2;
+            Real cf[NS];
+            if constexpr (COMPRESSED)
+              {
+                const Real *cg = prm.cell_geo + (long long)geo * NS;
+                Real wt = Real(1);
+                const int qa0 = p % K;
+                Real wa = Real(0);
+#pragma unroll
+                for (int i = 0; i < K; ++i)
+                  wa = (qa0 == i) ? tab<Real, K>(T::oW + i) : wa;
+                wt *= wa;
+                if constexpr (D == 3)
+                  {
+                    const int qa1 = p / K;
+                    wa = Real(0);
+#pragma unroll
+                    for (int i = 0; i < K; ++i)
+                      wa = (qa1 == i) ? tab<Real, K>(T::oW + i) : wa;
+                    wt *= wa;
+                  }
+                const Real w = wt * tab<Real, K>(T::oW + m);
+#pragma unroll
+                for (int e = 0; e < NS; ++e)
+                  cf[e] = __ldg(cg + e) * w;
+              }
+            else
+              {
+                const Real *cg = prm.cell_geo + (long long)geo * NS * NQ + p + P * m;
+#pragma unroll
+                for (int e = 0; e < NS; ++e)
+                  cf[e] = __ldcs(cg + e * NQ);
+              }
+            Real g[D];
+#pragma unroll
+            for (int b = 0; b < D; ++b)
+              g[b] = G[b * FS + q];
+            if constexpr (D == 3)
+              {
+                t[0] = cf[0] * g[0] + cf[3] * g[1] + cf[4] * g[2];
+                t[1] = cf[3] * g[0] + cf[1] * g[1] + cf[5] * g[2];
+                t[2] = cf[4] * g[0] + cf[5] * g[1] + cf[2] * g[2];
+              }
+            else
+              {
+                t[0] = cf[0] * g[0] + cf[2] * g[1];
+                t[1] = cf[2] * g[0] + cf[1] * g[1];
+              }
+          }
+        else if (geo >= 0)
           {
             Real jit[D * D], jw;
             if constexpr (COMPRESSED)

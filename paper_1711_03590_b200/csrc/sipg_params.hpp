@@ -26,6 +26,7 @@ struct ApplyParams
   const int2 *task_face;
   int n_tasks;
   int n_owned; // slots >= n_owned are ghost cells (ghost-side tasks)
+  int sym;     // 1: cell records hold the g4 coefficient [geo][d(d+1)/2][NQ]
 };
 
 // Advection apply (OperatorKind::advection, operators.cpp:634-667 cell,

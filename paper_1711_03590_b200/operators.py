@@ -242,7 +242,7 @@ class RankOperator:
         s.rank = rank
         s.config.d, s.config.p, s.config.W = config.d, config.p, config.W
         s.config.basis = BASIS_KINDS[config.basis]
-        s.config.geometry_variant = 3 if config.geometry == "g3" else -1
+        s.config.geometry_variant = {"g3": 3, "g4": 4}.get(config.geometry, -1)
         s.config.precision = {"fp64": 0, "fp32": 1}[config.precision]
         s.config.kind = 1 if config.kind == "advection" else 0
         for a in range(3):
@@ -265,7 +265,7 @@ class RankOperator:
             keep.append(a)
             g.compressed = int(bool(geometry.arrays.get("compressed", False)))
             for name in ("inv_jac_t", "jxw", "face_jxw", "face_jni", "face_jne",
-                         "penalty", "face_normal"):
+                         "penalty", "face_normal", "coeff"):
                 if name in a:
                     setattr(g, name, a[name].ctypes.data)
         h = C.c_void_p()

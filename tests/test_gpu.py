@@ -322,7 +322,8 @@ def test_apply_host_pointers(torch):
     assert rel_linf(y, c.g["y4"]) < TOL64
 
 
-@pytest.mark.parametrize("name", ["c5_cart_p6", "c3_vertex_p4", "c1_periodic_cart_p3", "c2_dirichlet_cart_p10"])
+@pytest.mark.parametrize("name", ["c5_cart_p6", "c3_vertex_p4", "c1_periodic_cart_p3", "c2_dirichlet_cart_p10",
+                                  "herm3d_p3_m2", "herm_c4_vertex_coef_p5_r2", "gauss2d_p2_periodic"])
 def test_fp32_against_fp64_reference(torch, name):
     c = Case(name)
     op, _ = build(c, n_ranks=1, precision="fp32")
@@ -645,3 +646,67 @@ def test_advection_rhs_against_reference(torch, field):
         ref = w.rhs(r)
         got = rhs.cpu().numpy()
         assert rel_linf(got, ref) < TOL64, rel_linf(got, ref)
+
+
+G4_CASES = [
+    # d, cells, p, amplitude, m, periodic, ranks, basis
+    (3, [3, 3, 3], 4, 0.05, 2, False, 1, "lagrange_gauss_lobatto"),
+    (3, [3, 2, 4], 5, 0.06, 3, False, 3, "hermite_like"),
+    (2, [5, 4], 6, 0.05, 2, True, 2, "lagrange_gauss_lobatto"),
+    (3, [4, 3, 3], 3, 0.0, 1, False, 1, "lagrange_gauss_lobatto"),
+    (3, [2, 2, 3], 2, 0.04, 2, True, 2, "lagrange_gauss"),
+]
+
+
+@pytest.mark.parametrize("cfg", G4_CASES, ids=lambda c: f"d{c[0]}p{c[2]}r{c[6]}-{c[7]}")
+def test_geometry_variant_g4_against_reference(torch, cfg):
+    """Geometry variant g4 (the merged coefficient J^{-1}J^{-T} det(J) w per
+    point, the paper's G4, geometry.cpp:219-246,370-388): device coefficient
+    bitwise equal to the reference precompute_geometry, apply equal to the
+    reference RankOperator with g4 at 1e-12."""
+    from oracle import reflib as R
+    if not R.available():
+        pytest.skip("reference library not built")
+    D = dgx()
+    d, cells, p, amp, m, periodic, nr, basis = cfg
+    w = R.World(d, cells, p, n_ranks=nr, amplitude=amp, mapping_degree=m, periodic=periodic,
+                basis=_RB[basis], variant="g4")
+    x = R.random_vector(w.n_dofs, 4000 + p)
+    y_ref = w.apply(x)
+    mesh = D.make_box_mesh(d, cells, amp, periodic, m)
+    faces = D.enumerate_faces(mesh)
+    part = D.partition_cells(mesh, nr)
+    D.assign_face_owners(mesh, faces, part)
+    cfg_ = D.OperatorConfig(d=d, p=p, basis=basis, geometry="g4")
+    ops = [D.RankOperator(mesh, part, faces, D.Geometry(source="mesh"), cfg_, r) for r in range(nr)]
+    if nr == 1:
+        ns = d * (d + 1) // 2
+        nrec = 1 if amp == 0.0 else (p + 1) ** d
+        mine = ops[0].device_geometry(0).reshape(-1, ns, nrec).transpose(0, 2, 1).ravel()
+        assert np.array_equal(mine, w.geometry("coeff"))
+        y = apply_single(torch, ops[0], x)
+    else:
+        y = apply_serial_ranks(torch, ops, None, x, (p + 1) ** d,
+                               planned_only=basis == "hermite_like")
+    assert rel_linf(y, y_ref) < TOL64 and rel_l2(y, y_ref) < TOL64, (rel_linf(y, y_ref),)
+
+
+def test_geometry_variant_g4_host_arrays(torch):
+    """g4 from the reference's GeometryCache arrays (DGX_GEOMETRY_HOST_ARRAYS)."""
+    from oracle import reflib as R
+    if not R.available():
+        pytest.skip("reference library not built")
+    D = dgx()
+    d, cells, p = 3, [3, 3, 2], 4
+    w = R.World(d, cells, p, amplitude=0.05, mapping_degree=2, variant="g4")
+    x = R.random_vector(w.n_dofs, 77)
+    mesh = D.make_box_mesh(d, cells, 0.05, False, 2)
+    faces = D.enumerate_faces(mesh)
+    part = D.partition_cells(mesh, 1)
+    D.assign_face_owners(mesh, faces, part)
+    arrays = {k: w.geometry(k) for k in ("coeff", "face_jxw", "face_jni", "face_jne", "penalty")}
+    arrays["compressed"] = False
+    op = D.RankOperator(mesh, part, faces, D.Geometry(source="host_arrays", arrays=arrays),
+                        D.OperatorConfig(d=d, p=p, geometry="g4"), 0)
+    y = apply_single(torch, op, x)
+    assert rel_linf(y, w.apply(x)) < TOL64
