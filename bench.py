@@ -60,6 +60,11 @@ CONFIGS = {
 CONFIGS["a4"] = (3, 128, 5, False, "mesh", False, "fp64", 3,
                  "A4: 3D advection, deformed 128^3 (reference mapping m=2), p=5, c=(0.85,0.6,0.35), fp64")
 ADVECTION = {"a4": (0.85, 0.6, 0.35)}
+# the paper's geometry variant G4 (merged coefficient, 6 instead of 10
+# doubles per point) on the C3 / C4 workloads
+CONFIGS["c4g4"] = CONFIGS["c4"][:8] + ("C4g4: C4 with geometry variant g4 (merged coefficient)",)
+CONFIGS["c3g4"] = CONFIGS["c3"][:8] + ("C3g4: C3 with geometry variant g4 (merged coefficient)",)
+VARIANT = {"c4g4": "g4", "c3g4": "g4"}
 # BasisKind per config (default: the nodal Gauss-Lobatto basis BASELINE names)
 BASIS = {"c4h": "hermite_like", "c3h": "hermite_like", "c5h": "hermite_like"}
 # reference instrumented flop count per DoF (counters x W / applies,
@@ -67,7 +72,8 @@ BASIS = {"c4h": "hermite_like", "c3h": "hermite_like", "c5h": "hermite_like"}
 REF_FLOPS_PER_DOF = {"c4": 240.0, "c3": 215.52, "c5": 260.82, "c5f32": 260.82,
                      "c1": 198.0, "c2": 105.80,
                      # Hermite-like: plain (not even-odd) S passes, same counters
-                     "c4h": 268.0, "c3h": 242.4, "c5h": 293.14, "a4": 93.0}
+                     "c4h": 268.0, "c3h": 242.4, "c5h": 293.14, "a4": 93.0,
+                     "c4g4": 240.0, "c3g4": 215.52}
 
 
 def peaks():
@@ -183,7 +189,8 @@ class RefBench:
                         amplitude=0.05 if kind == "mesh" else 0.0,
                         mapping_degree=2 if kind == "mesh" else 1,
                         kind="advection" if adv else "laplacian",
-                        velocity=adv or (1.0, 1.0, 1.0))
+                        velocity=adv or (1.0, 1.0, 1.0),
+                        variant=VARIANT.get(cfg_name, "g3"))
             w.time(1)
             t = min(w.time(1) for _ in range(3))
             if best is None or t < best[0]:
@@ -230,6 +237,7 @@ def main():
               else "DG Laplacian apply throughput (DoFs/s)")
     config = {"workload": label, "cells": [n] * d, "degree": p, "n_dofs": n_dofs,
               "basis": BASIS.get(args.config, "lagrange_gauss_lobatto"),
+              "geometry_variant": VARIANT.get(args.config, "g3"),
               "seed": seed, "partition": f"contiguous lexicographic slabs x{args.gpus}",
               "l2": "inputs larger than L2 (no flush)"}
 
@@ -273,7 +281,8 @@ def main():
     adv = ADVECTION.get(args.config)
     op = dgx.RankOperator(mesh, part, faces, geo, dgx.OperatorConfig(
         d=d, p=p, precision=prec, basis=BASIS.get(args.config, "lagrange_gauss_lobatto"),
-        kind="advection" if adv else "laplacian", velocity=adv or (1.0, 1.0, 1.0)),
+        kind="advection" if adv else "laplacian", velocity=adv or (1.0, 1.0, 1.0),
+        geometry=VARIANT.get(args.config, "g3")),
         rank, device=local)
     lay = op.layout()
     hooks = None

@@ -314,7 +314,7 @@ int dgref_world_create_ext(int d, const int *cells, int periodic, int p,
     g->k = k;
     g->l = k;
     g->equation = Equation::laplacian;
-    g->variant = GeometryVariant::g3;
+    g->variant = w->cfg.geometry; // g3, or g4 (dgref_set_variant)
     g->compression = compressed ? GeometryCompression::cartesian
                                 : GeometryCompression::general;
     g->quad1d = gauss_quadrature(k);
@@ -350,6 +350,24 @@ int dgref_world_create_ext(int d, const int *cells, int periodic, int p,
     const long long nrec = static_cast<long long>(g->n_cells) * g->n_q_cell;
     g->inv_jac_t.assign(inv_jac_t, inv_jac_t + nrec * d * d);
     g->jxw.assign(jxw, jxw + nrec);
+    if (g->variant == GeometryVariant::g4)
+      {
+        // the merged coefficient of the injected g3 data, formed exactly as
+        // precompute_geometry does (symmetric_coefficient, geometry.cpp:219-246)
+        const int ns = n_symmetric_entries(d);
+        const int ii[6] = {0, 1, 2, 0, 0, 1}, jj[6] = {0, 1, 2, 1, 2, 2};
+        const int ii2[3] = {0, 1, 0}, jj2[3] = {0, 1, 1};
+        g->coeff.resize(nrec * ns);
+        for (long long r = 0; r < nrec; ++r)
+          for (int e = 0; e < ns; ++e)
+            {
+              const int i = d == 3 ? ii[e] : ii2[e], j = d == 3 ? jj[e] : jj2[e];
+              double s = 0;
+              for (int a = 0; a < d; ++a)
+                s += inv_jac_t[r * d * d + a * d + i] * inv_jac_t[r * d * d + a * d + j];
+              g->coeff[r * ns + e] = s * jxw[r];
+            }
+      }
     const long long nf = g->n_faces * g->n_q_face;
     g->face_jxw.assign(face_jxw, face_jxw + nf);
     g->face_jni.assign(face_jni, face_jni + nf * d);

@@ -450,11 +450,14 @@ __global__ void __launch_bounds__(KernelShape<D, K>::THREADS, KernelShape<D, K>:
   if (active)
     {
       constexpr int LINE = 128;
+      // doubles per point of the cell record: g3 J^{-T} + JxW, g4 the
+      // merged symmetric coefficient
+      const int ncg = prm.sym ? D * (D + 1) / 2 : D * D + 1;
       if (geo >= 0)
         {
           const char *gp = reinterpret_cast<const char *>(
-            prm.cell_geo + (long long)geo * (D * D + 1) * (COMPRESSED ? 1 : NQ));
-          constexpr int bytes = (D * D + 1) * (COMPRESSED ? 1 : NQ) * (int)sizeof(Real);
+            prm.cell_geo + (long long)geo * ncg * (COMPRESSED ? 1 : NQ));
+          const int bytes = ncg * (COMPRESSED ? 1 : NQ) * (int)sizeof(Real);
           for (int off = p * LINE; off < bytes; off += P * LINE)
             asm volatile("prefetch.global.L2 [%0];" ::"l"(gp + off));
         }
