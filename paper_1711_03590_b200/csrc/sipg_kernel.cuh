@@ -453,7 +453,10 @@ __global__ void __launch_bounds__(KernelShape<D, K>::THREADS, KernelShape<D, K>:
       // doubles per point of the cell record: g3 J^{-T} + JxW, g4 the
       // merged symmetric coefficient
       const int ncg = prm.sym ? D * (D + 1) / 2 : D * D + 1;
-      if (geo >= 0)
+#ifndef DGX_EXP_PF
+#define DGX_EXP_PF 3 // bit 0: cell record, bit 1: face records, bit 2: neighbours (measured: bits 0+1 best, neighbour prefetch costs 2%)
+#endif
+      if ((DGX_EXP_PF & 1) && geo >= 0)
         {
           const char *gp = reinterpret_cast<const char *>(
             prm.cell_geo + (long long)geo * ncg * (COMPRESSED ? 1 : NQ));
@@ -469,15 +472,16 @@ __global__ void __launch_bounds__(KernelShape<D, K>::THREADS, KernelShape<D, K>:
       for (int phi = 0; phi < 2 * D; ++phi)
         {
           const int2 tf = prm.task_face[task * 2 * D + phi];
-          if (tf.x == -2)
+          if (tf.x == -2 || !(DGX_EXP_PF & 6))
             continue;
           constexpr int FREC = COMPRESSED ? 1 : P;
           const char *fp = reinterpret_cast<const char *>(
             prm.face_geo + (long long)(tf.y & 0x3fffffff) * (2 * D + 1) * FREC);
           constexpr int fbytes = (2 * D + 1) * FREC * (int)sizeof(Real);
-          for (int off = p * LINE; off < fbytes; off += P * LINE)
-            asm volatile("prefetch.global.L2 [%0];" ::"l"(fp + off));
-          if (tf.x >= 0)
+          if (DGX_EXP_PF & 2)
+            for (int off = p * LINE; off < fbytes; off += P * LINE)
+              asm volatile("prefetch.global.L2 [%0];" ::"l"(fp + off));
+          if ((DGX_EXP_PF & 4) && tf.x >= 0)
             {
               const char *np = reinterpret_cast<const char *>(prm.u + (long long)tf.x * NQ);
               constexpr int nbytes = NQ * (int)sizeof(Real);
