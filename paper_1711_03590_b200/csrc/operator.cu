@@ -576,6 +576,7 @@ void Operator::launch_range(int begin, int count, const Real *u, Real *y, cudaSt
   prm.n_tasks = count;
   prm.n_owned = static_cast<int>(layout_.n_owned);
   prm.sym = sym_ ? 1 : 0;
+  prm.ahead = 0;
   launch_apply<Real>(d_, k_, basis_, compressed_, prm, s);
 }
 

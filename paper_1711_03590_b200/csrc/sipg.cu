@@ -3,6 +3,7 @@
 // sipg_gl.cu, sipg_gauss.cu and sipg_hermite.cu (sipg_launch.cuh).
 #include "device.hpp"
 #include "sipg_kernel.cuh"
+#include "sipg_pairs.cuh"
 
 namespace dgx
 {
@@ -36,7 +37,7 @@ int kernel_cells_per_cta(int D, int K)
 {
 #define DGX_NC(DD, KK)                                                                     \
   if (D == DD && K == KK)                                                                  \
-    return dev::KernelShape<DD, KK>::NC;
+    return (DD == 3 && KK % 2 == 0) ? dev::PL<KK>::NC : dev::KernelShape<DD, KK>::NC;
   DGX_NC(2, 2) DGX_NC(2, 3) DGX_NC(2, 4) DGX_NC(2, 5) DGX_NC(2, 6) DGX_NC(2, 7)
   DGX_NC(2, 8) DGX_NC(2, 9) DGX_NC(2, 10) DGX_NC(2, 11)
   DGX_NC(3, 2) DGX_NC(3, 3) DGX_NC(3, 4) DGX_NC(3, 5) DGX_NC(3, 6) DGX_NC(3, 7)
@@ -87,6 +88,13 @@ template void launch_apply<double>(int, int, int, bool, const dev::ApplyParams<d
 #ifdef DGX_WITH_FP32
 template void launch_apply<float>(int, int, int, bool, const dev::ApplyParams<float> &,
                                   cudaStream_t);
+#elif defined(DGX_DEV_K)
+// kernel-experiment builds are fp64 only
+template <>
+void launch_apply<float>(int, int, int, bool, const dev::ApplyParams<float> &, cudaStream_t)
+{
+  fail(Code::invalid_argument, "fp32 apply not built (DGX_DEV_K experiment build)");
+}
 #endif
 
 } // namespace dgx

@@ -420,23 +420,16 @@ namespace dev
 // bases) the neighbour's whole pencil. BASIS is a template argument also so
 // that the instantiations of the per-basis translation units (each with its
 // own constant tables) are distinct kernels, not one weak host stub.
+// One task (cell slot) per group of P threads.
 template <typename Real, int D, int K, bool COMPRESSED, int BASIS>
-__global__ void __launch_bounds__(KernelShape<D, K>::THREADS, KernelShape<D, K>::MIN_BLOCKS)
-  sipg_apply_kernel(const ApplyParams<Real> prm)
+__device__ __forceinline__ void sipg_task(const ApplyParams<Real> &prm, Real *cell, int p,
+                                          int task)
 {
   constexpr bool HERM = BASIS == 2;
-  using KS = KernelShape<D, K>;
   using L = SL<D, K>;
   using T = TabLayout<K>;
-  constexpr int P = L::P, NQ = L::NQ, NC = KS::NC, FS = L::FS;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  Real *smem = reinterpret_cast<Real *>(smem_raw);
-
-  const int lc = threadIdx.x / P;
-  const int p = threadIdx.x - lc * P;
-  const int task = blockIdx.x * NC + lc;
+  constexpr int P = L::P, NQ = L::NQ, FS = L::FS;
   const bool active = task < prm.n_tasks;
-  Real *cell = smem + lc * L::SM_CELL;
   Real *val = cell;
   Real *G = cell + L::OFF_G;
 
@@ -790,6 +783,21 @@ __global__ void __launch_bounds__(KernelShape<D, K>::THREADS, KernelShape<D, K>:
           }
       }
   }
+}
+
+template <typename Real, int D, int K, bool COMPRESSED, int BASIS>
+__global__ void __launch_bounds__(KernelShape<D, K>::THREADS, KernelShape<D, K>::MIN_BLOCKS)
+  sipg_apply_kernel(const ApplyParams<Real> prm)
+{
+  using KS = KernelShape<D, K>;
+  using L = SL<D, K>;
+  constexpr int P = L::P, NC = KS::NC;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  Real *smem = reinterpret_cast<Real *>(smem_raw);
+  const int lc = threadIdx.x / P;
+  const int p = threadIdx.x - lc * P;
+  Real *cell = smem + lc * L::SM_CELL;
+  sipg_task<Real, D, K, COMPRESSED, BASIS>(prm, cell, p, blockIdx.x * NC + lc);
 }
 
 } // namespace dev

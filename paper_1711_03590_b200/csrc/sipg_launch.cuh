@@ -7,6 +7,7 @@
 #include "device.hpp"
 #include "setup.hpp"
 #include "sipg_kernel.cuh"
+#include "sipg_pairs.cuh"
 #include "sipg_rhs.cuh"
 #include "sipg_adv.cuh"
 
@@ -98,9 +99,49 @@ std::vector<double> build_table(int K)
 std::mutex g_mutex;
 std::set<std::tuple<int, int>> g_uploaded; // (device, K)
 
+template <typename KERN>
+void set_smem_once(KERN kern, size_t smem, std::set<int> &configured);
+
+#ifndef DGX_PAIRS
+#define DGX_PAIRS 1 // 3D, even K, fp64: the pencil-pair kernel (sipg_pairs.cuh)
+#endif
+
+template <int K, bool C>
+void launch_pairs(const dev::ApplyParams<double> &prm, cudaStream_t s)
+{
+  using L = dev::PL<K>;
+  const size_t smem = (size_t)L::SMEM_REALS * sizeof(double);
+  auto kern = dev::sipg_pairs_kernel<K, C, DGX_BASIS>;
+  static std::set<int> configured;
+  set_smem_once(kern, smem, configured);
+  static int resident[64] = {0}; // CTAs resident on the whole device, per device
+  int devid = 0;
+  cuda_check(cudaGetDevice(&devid), "cudaGetDevice");
+  if (devid >= 0 && devid < 64 && resident[devid] == 0)
+    {
+      int per_sm = 0, sms = 0;
+      cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, L::THREADS, smem),
+                 "cudaOccupancyMaxActiveBlocksPerMultiprocessor");
+      cuda_check(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, devid),
+                 "cudaDeviceGetAttribute");
+      resident[devid] = per_sm * sms > 0 ? per_sm * sms : 1;
+    }
+  dev::ApplyParams<double> p2 = prm;
+  p2.ahead = ((devid >= 0 && devid < 64) ? resident[devid] : 1) * L::NC;
+  const int grid = (prm.n_tasks + L::NC - 1) / L::NC;
+  if (grid > 0)
+    kern<<<grid, L::THREADS, smem, s>>>(p2);
+  cuda_check(cudaGetLastError(), "sipg_pairs_kernel launch");
+}
+
 template <typename Real, int D, int K, bool C>
 void launch_one(const dev::ApplyParams<Real> &prm, cudaStream_t s)
 {
+  if constexpr (DGX_PAIRS && D == 3 && K % 2 == 0 && sizeof(Real) == 8)
+    {
+      launch_pairs<K, C>(prm, s);
+      return;
+    }
   using KS = dev::KernelShape<D, K>;
   const size_t smem = (size_t)KS::SMEM_REALS * sizeof(Real);
   auto kern = dev::sipg_apply_kernel<Real, D, K, C, DGX_BASIS>;
@@ -140,6 +181,13 @@ void launch_d(int K, bool compressed, const dev::ApplyParams<Real> &prm, cudaStr
 {
   switch (K)
     {
+#ifdef DGX_DEV_K
+    // kernel-experiment builds (tools/expbuild.sh): one 3D degree only
+    case DGX_DEV_K:
+      if constexpr (D == 3)
+        launch_k<Real, D, DGX_DEV_K>(compressed, prm, s);
+      break;
+#else
 #if DGX_BASIS != 2
     case 2: launch_k<Real, D, 2>(compressed, prm, s); break;
     case 3: launch_k<Real, D, 3>(compressed, prm, s); break;
@@ -152,6 +200,7 @@ void launch_d(int K, bool compressed, const dev::ApplyParams<Real> &prm, cudaStr
     case 9: launch_k<Real, D, 9>(compressed, prm, s); break;
     case 10: launch_k<Real, D, 10>(compressed, prm, s); break;
     case 11: launch_k<Real, D, 11>(compressed, prm, s); break;
+#endif
     default: fail(Code::invalid_argument, "sipg apply: unsupported k");
     }
 }
@@ -200,8 +249,12 @@ void launch_adv_d(int K, bool compressed, const dev::AdvParams<double> &prm, cud
     else                                                                                   \
       launch_adv_one<D, KK, false>(prm, s);                                                \
     break;
+#ifdef DGX_DEV_K
+      DGX_ADV_K(DGX_DEV_K)
+#else
       DGX_ADV_K(2) DGX_ADV_K(3) DGX_ADV_K(4) DGX_ADV_K(5) DGX_ADV_K(6) DGX_ADV_K(7)
       DGX_ADV_K(8) DGX_ADV_K(9) DGX_ADV_K(10) DGX_ADV_K(11)
+#endif
 #undef DGX_ADV_K
     default: fail(Code::invalid_argument, "advection: unsupported k");
     }
@@ -244,11 +297,15 @@ void launch_rhs_d(int K, bool compressed, const dev::RhsParams<double> &prm, cud
     else                                                                                   \
       launch_rhs_one<D, KK, false, ADV>(prm, s);                                           \
     break;
+#ifdef DGX_DEV_K
+      DGX_RHS_K(DGX_DEV_K)
+#else
 #if DGX_BASIS != 2
       DGX_RHS_K(2) DGX_RHS_K(3)
 #endif
       DGX_RHS_K(4) DGX_RHS_K(5) DGX_RHS_K(6) DGX_RHS_K(7) DGX_RHS_K(8) DGX_RHS_K(9)
       DGX_RHS_K(10) DGX_RHS_K(11)
+#endif
 #undef DGX_RHS_K
     default: fail(Code::invalid_argument, "assemble_rhs: unsupported k");
     }
