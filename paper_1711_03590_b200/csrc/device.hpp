@@ -96,6 +96,8 @@ struct AdvParams;
 // basis: 0 lagrange_gauss_lobatto, 1 lagrange_gauss, 2 hermite_like
 void upload_tables(int K, int basis);
 int kernel_cells_per_cta(int D, int K);
+// brick size of the pencil-pair kernel's CTAs (0: none; 4: 2x2x1; 8: 2x2x2)
+int kernel_brick(int D, int K);
 template <typename Real>
 void launch_apply(int D, int K, int basis, bool compressed, const dev::ApplyParams<Real> &prm,
                   cudaStream_t s);

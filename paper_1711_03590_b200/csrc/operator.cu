@@ -191,41 +191,93 @@ void Operator::build_tasks(const std::vector<RawFace> &faces, const Partition &p
   // z inside tiles of full x-rows and TILE_Y y-rows instead: the z-neighbour
   // (and the shared face record) is then n_x TILE_Y tasks away and still in
   // L2; only neighbours across the y tile edges are read twice from HBM.
-  std::vector<long long> order;
-  order.reserve(n_owned);
+  //
+  // Brick CTAs (the pencil-pair kernel, sipg_pairs.cuh): the same sweep in
+  // 2x2x2 (or 2x2x1) bricks of consecutive tasks, one brick per CTA, so that
+  // the faces inside a brick take the partner's trace from shared memory.
+  // A brick goes whole into one phase list (coupled if any of its cells
+  // reads a ghost) so that the CTA groups stay aligned; cells of incomplete
+  // bricks follow as single tasks.
+  std::vector<std::vector<long long>> groups;
   {
     const int nx = mesh_.cells[0], ny = d_ == 3 ? mesh_.cells[1] : 1;
     const long long layer = (long long)nx * ny;
     const long long b = layout_.owned_begin, e = b + n_owned;
     const int tile_y = d_ == 3 ? 8 : 1 << 30;
-    if (d_ == 3)
+    const int brick0 = (d_ == 3 && precision_ == 0) ? kernel_brick(d_, k_) : 0;
+    const int brick = brick0 >= 4 ? brick0 : 0; // 1: x-rows, no reordering
+    auto in_range = [&](long long z, int y, int x) {
+      const long long c = z * layer + (long long)y * nx + x;
+      return x < nx && y < ny && c >= b && c < e;
+    };
+    if (d_ == 3 && brick > 0)
+      {
+        const int bz = brick == 8 ? 2 : 1;
+        std::vector<char> used(n_owned, 0);
+        const long long z0 = b / layer, z1 = (e + layer - 1) / layer;
+        for (int ty = 0; ty < ny; ty += tile_y)
+          for (long long z = z0; z < z1; z += bz)
+            for (int y = ty; y < std::min(ny, ty + tile_y); y += 2)
+              for (int x = 0; x < nx; x += 2)
+                {
+                  std::vector<long long> g;
+                  for (int iz = 0; iz < bz; ++iz)
+                    for (int iy = 0; iy < 2; ++iy)
+                      for (int ix = 0; ix < 2; ++ix)
+                        if (y + iy < std::min(ny, ty + tile_y) && in_range(z + iz, y + iy, x + ix))
+                          g.push_back((z + iz) * layer + (long long)(y + iy) * nx + x + ix - b);
+                  if ((int)g.size() == brick)
+                    {
+                      for (long long c : g)
+                        used[c] = 1;
+                      groups.push_back(g);
+                    }
+                }
+        for (int ty = 0; ty < ny; ty += tile_y)
+          for (long long z = z0; z < z1; ++z)
+            for (int y = ty; y < std::min(ny, ty + tile_y); ++y)
+              for (int x = 0; x < nx; ++x)
+                if (in_range(z, y, x))
+                  {
+                    const long long c = z * layer + (long long)y * nx + x - b;
+                    if (!used[c])
+                      groups.push_back({c});
+                  }
+      }
+    else if (d_ == 3)
       {
         const long long z0 = b / layer, z1 = (e + layer - 1) / layer;
         for (int ty = 0; ty < ny; ty += tile_y)
           for (long long z = z0; z < z1; ++z)
             for (int y = ty; y < std::min(ny, ty + tile_y); ++y)
               for (int x = 0; x < nx; ++x)
-                {
-                  const long long c = z * layer + (long long)y * nx + x;
-                  if (c >= b && c < e)
-                    order.push_back(c - b);
-                }
+                if (in_range(z, y, x))
+                  groups.push_back({z * layer + (long long)y * nx + x - b});
       }
     else
       for (long long s = 0; s < n_owned; ++s)
-        order.push_back(s);
+        groups.push_back({s});
   }
-  for (long long s : order)
-    {
-      std::vector<int2> tf;
-      const bool coupled = make_task(s, true, tf);
-      auto &sl = coupled ? slot_coupled : slot_inner;
-      auto &gl = coupled ? geo_coupled : geo_inner;
-      auto &fl = coupled ? tf_coupled : tf_inner;
-      sl.push_back(static_cast<int>(s));
-      gl.push_back(static_cast<int>(s));
-      fl.insert(fl.end(), tf.begin(), tf.end());
-    }
+  // whole bricks first in each phase list, single tasks after them
+  for (int pass = 0; pass < 2; ++pass)
+    for (const auto &g : groups)
+      {
+        if ((pass == 0) != (g.size() > 1))
+          continue;
+        std::vector<std::vector<int2>> tfs(g.size());
+        bool coupled = false;
+        for (std::size_t i = 0; i < g.size(); ++i)
+          coupled = make_task(g[i], true, tfs[i]) || coupled;
+        auto &sl = coupled ? slot_coupled : slot_inner;
+        auto &gl = coupled ? geo_coupled : geo_inner;
+        auto &fl = coupled ? tf_coupled : tf_inner;
+        for (std::size_t i = 0; i < g.size(); ++i)
+          {
+            sl.push_back(static_cast<int>(g[i]));
+            gl.push_back(static_cast<int>(g[i]));
+            fl.insert(fl.end(), tfs[i].begin(), tfs[i].end());
+          }
+      }
   for (long long s = n_owned; s < n_slots; ++s)
     {
       std::vector<int2> tf;

@@ -46,6 +46,21 @@ int kernel_cells_per_cta(int D, int K)
   return 1;
 }
 
+int kernel_brick(int D, int K)
+{
+#if defined(DGX_PAIRS) && !DGX_PAIRS
+  (void)D, (void)K;
+  return 0;
+#else
+#define DGX_BR(KK)                                                                         \
+  if (D == 3 && K == KK)                                                                   \
+    return dev::PL<KK>::BRICK;
+  DGX_BR(4) DGX_BR(6) DGX_BR(8) DGX_BR(10)
+#undef DGX_BR
+  return 0;
+#endif
+}
+
 template <typename Real>
 void launch_apply(int D, int K, int basis, bool compressed, const dev::ApplyParams<Real> &prm,
                   cudaStream_t s)

@@ -59,15 +59,31 @@ struct PL
 #else
   static constexpr int G = P2;
 #endif
-  static constexpr int SM_CELL = pr_stride(OFF_TF + 6, G);
+  static constexpr int SM_CELL = pr_stride(OFF_TF + 7, G); // + the task's slot
   static constexpr int NC_THREADS = (160 / G) > 0 ? 160 / G : 1;
+  static constexpr int NC_SMEM = (74 * 1024 / 8) / SM_CELL > 0 ? (74 * 1024 / 8) / SM_CELL : 1;
+  // Brick CTAs: the CTA's cells form a 2x2x2 (BRICK 8) or 2x2x1 (BRICK 4)
+  // brick of the task order (Operator::build_tasks); a face between two
+  // cells of the brick takes the partner's own trace from shared memory
+  // instead of re-evaluating it from the partner's nodal values.
+#ifndef DGX_PAIRS_BRICK
+#define DGX_PAIRS_BRICK 1 // measured (C4, 21.6 -> 21.1 ms); 2x2x2 and 2x2x1 bricks need NC = 8 or 4: slower (23.6, 22.1 ms)
+#endif
+  // BRICK 1: no reordering; consecutive tasks of the CTA that are
+  // x-neighbours (the tiled task order runs along x) share their x-face.
+  static constexpr int BRICK = (DGX_PAIRS_BRICK == 1 || (DGX_PAIRS_BRICK > 1 && DGX_PAIRS_BRICK * SM_CELL * 8 <= 113 * 1024))
+                                 ? DGX_PAIRS_BRICK : 0;
 #ifdef DGX_PAIRS_NC
   static constexpr int NC = DGX_PAIRS_NC;
 #else
-  static constexpr int NC_SMEM = (74 * 1024 / 8) / SM_CELL > 0 ? (74 * 1024 / 8) / SM_CELL : 1;
-  static constexpr int NC = NC_THREADS < NC_SMEM ? NC_THREADS : NC_SMEM;
+  static constexpr int NC = BRICK > 1 ? BRICK : (NC_THREADS < NC_SMEM ? NC_THREADS : NC_SMEM);
 #endif
   static constexpr int THREADS = NC * G;
+#ifdef DGX_PAIRS_MINB
+  static constexpr int MINB = DGX_PAIRS_MINB;
+#else
+  static constexpr int MINB = (220 * 1024) / (NC * SM_CELL * 8 + 1024) >= 3 ? 3 : 2; // CTAs per SM
+#endif
   static constexpr int SMEM_REALS = NC * SM_CELL;
 };
 
@@ -163,6 +179,37 @@ __device__ __forceinline__ void pr_ldg(const double *f, int c, int w, double (&x
     }
 }
 
+// predicated variant (branch-free: the loads of both faces stay in flight
+// together); zeros where !pred
+template <int K, int A, int PS>
+__device__ __forceinline__ void pr_ldg_if(bool pred, const double *f, int c, int w, double (&x)[2][K])
+{
+  const double2 z = make_double2(0.0, 0.0);
+  if constexpr (A == 0)
+    {
+#pragma unroll
+      for (int e = 0; e < 2; ++e)
+#pragma unroll
+        for (int j = 0; j < K / 2; ++j)
+          {
+            const double2 v =
+              pred ? __ldg(reinterpret_cast<const double2 *>(f + pr_el<K, A, PS>(c, w, e, 2 * j))) : z;
+            x[e][2 * j] = v.x;
+            x[e][2 * j + 1] = v.y;
+          }
+    }
+  else
+    {
+#pragma unroll
+      for (int m = 0; m < K; ++m)
+        {
+          const double2 v = pred ? __ldg(reinterpret_cast<const double2 *>(f + pr_el<K, A, PS>(c, w, 0, m))) : z;
+          x[0][m] = v.x;
+          x[1][m] = v.y;
+        }
+    }
+}
+
 // elements m and m+1 of both pencils of the pair along A (global)
 template <int K, int A>
 __device__ __forceinline__ void pr_ldg_two(const double *f, int c, int w, int m, double (&lo)[2],
@@ -241,10 +288,10 @@ __device__ __forceinline__ void pr_face_terms(const double *cell, int c, int w, 
 // Both faces of axis A (same algebra as face_axis_v4, sipg_faces.cuh, with
 // the pair mapping): own traces, neighbour trace, SIPG flux
 // (operators.cpp:977-1003 interior, 1069-1089 boundary), test side.
-template <int K, int A, bool COMPRESSED, bool HERM>
+template <int K, int A, bool COMPRESSED, bool HERM, typename HOOK>
 __device__ __forceinline__ void pr_face_axis(const ApplyParams<double> &prm, double *cell, bool active,
-                                             int c, int w, int t, const double (&wf)[2],
-                                             const double (&sp)[2])
+                                             int c, int w, int t, int lc, const double (&wf)[2],
+                                             const double (&sp)[2], HOOK &&before_wpass)
 {
   using L = PL<K>;
   using T = TabLayout<K>;
@@ -264,6 +311,34 @@ __device__ __forceinline__ void pr_face_axis(const ApplyParams<double> &prm, dou
       tf[0] = tfs[2 * A];
       tf[1] = tfs[2 * A + 1];
     }
+  // face shared with the brick partner along A (its own trace and normal
+  // derivative are in its NB slots of the opposite side after the barrier)
+  bool inr[2] = {false, false};
+  const double *PNB[2] = {NB, NB};
+  if constexpr (L::BRICK == 8 || (L::BRICK == 4 && A < 2))
+    {
+      const int lp = lc ^ (1 << A);
+      const double *pcell = cell + (lp - lc) * L::SM_CELL;
+      PNB[0] = PNB[1] = pcell + L::OFF_NB;
+      const int pslot = reinterpret_cast<const int *>(pcell + L::OFF_TF)[12];
+#pragma unroll
+      for (int s = 0; s < 2; ++s)
+        inr[s] = tf[s].x >= 0 && tf[s].x == pslot;
+    }
+  if constexpr (L::BRICK == 1 && A == 0)
+    {
+#pragma unroll
+      for (int s = 0; s < 2; ++s)
+        {
+          const int lp = lc + (s == 0 ? -1 : 1);
+          if (lp >= 0 && lp < L::NC)
+            {
+              const double *pcell = cell + (lp - lc) * L::SM_CELL;
+              PNB[s] = pcell + L::OFF_NB;
+              inr[s] = tf[s].x >= 0 && tf[s].x == reinterpret_cast<const int *>(pcell + L::OFF_TF)[12];
+            }
+        }
+    }
   // neighbour nodal value / normal-derivative layers at the two points
   if constexpr (HERM)
     {
@@ -274,7 +349,7 @@ __device__ __forceinline__ void pr_face_axis(const ApplyParams<double> &prm, dou
 #pragma unroll
           for (int e = 0; e < 2; ++e)
             xe[s][e] = xi[s][e] = 0.0;
-          if (tf[s].x >= 0)
+          if (tf[s].x >= 0 && !inr[s])
             {
               const double *un = prm.u + (long long)tf[s].x * NQ;
               if (s == 0)
@@ -307,14 +382,18 @@ __device__ __forceinline__ void pr_face_axis(const ApplyParams<double> &prm, dou
 #pragma unroll
       for (int s = 0; s < 2; ++s)
         {
-          const double *un = prm.u + (long long)(tf[s].x >= 0 ? tf[s].x : 0) * NQ;
-          pr_ldg<K, A, K * K>(un, c, w, x[s]);
+#ifdef DGX_NBLOAD_OLD
+          pr_ldg<K, A, K * K>(prm.u + (long long)(tf[s].x >= 0 ? tf[s].x : 0) * NQ, c, w, x[s]);
           if (tf[s].x < 0)
 #pragma unroll
             for (int e = 0; e < 2; ++e)
 #pragma unroll
               for (int m = 0; m < K; ++m)
                 x[s][e][m] = 0.0;
+#else
+          pr_ldg_if<K, A, K * K>(tf[s].x >= 0 && !inr[s], prm.u + (long long)(tf[s].x >= 0 ? tf[s].x : 0) * NQ,
+                                 c, w, x[s]);
+#endif
         }
       sts2(NB + fp, dot_row<double, K, T::oSf + K>(x[0][0]), dot_row<double, K, T::oSf + K>(x[0][1]));
       sts2(NB + FP + fp, dot_row<double, K, T::oDf + K>(x[0][0]), dot_row<double, K, T::oDf + K>(x[0][1]));
@@ -384,6 +463,12 @@ __device__ __forceinline__ void pr_face_axis(const ApplyParams<double> &prm, dou
       for (int e = 0; e < 2; ++e)
         dn_own[s][e] = own_g[s][e][0] * jo[s][e][0] + own_g[s][e][1] * jo[s][e][1] +
                        own_g[s][e][2] * jo[s][e][2];
+      if (inr[s])
+        {
+          // n^- . J^{-T} grad u on this side: the partner's neighbour term
+          sts2(NB + (2 * s) * FP + fp, own_u[s][0], own_u[s][1]);
+          sts2(NB + (2 * s + 1) * FP + fp, dn_own[s][0], dn_own[s][1]);
+        }
     }
   __syncthreads();
 
@@ -391,6 +476,8 @@ __device__ __forceinline__ void pr_face_axis(const ApplyParams<double> &prm, dou
   for (int tk = t; tk < 4 * H; tk += L::G)
     {
       const int a = tk / 4, f = tk - a * 4; // field fastest (conflict-free)
+      if ((f < 2) ? inr[0] : inr[1])
+        continue;
       double *fld = NB + f * FP + 2 * a;
       double x[2][K], y[2][K];
 #pragma unroll
@@ -457,9 +544,11 @@ __device__ __forceinline__ void pr_face_axis(const ApplyParams<double> &prm, dou
               jxw[s][0] = j2.x;
               jxw[s][1] = j2.y;
 #pragma unroll
+#pragma unroll
               for (int b = 0; b < 3; ++b)
                 {
-                  const double2 n = __ldg(reinterpret_cast<const double2 *>(fg + (1 + (1 - side) * 3 + b) * P));
+                  const double2 n = !inr[s] ? __ldg(reinterpret_cast<const double2 *>(fg + (1 + (1 - side) * 3 + b) * P))
+                                            : make_double2(0.0, 0.0);
                   jb[s][0][b] = n.x;
                   jb[s][1][b] = n.y;
                 }
@@ -471,6 +560,8 @@ __device__ __forceinline__ void pr_face_axis(const ApplyParams<double> &prm, dou
   for (int tk = t; tk < 6 * K; tk += L::G)
     {
       const int f = tk / K, r = tk - f * K;
+      if ((f < 2 || f == 4) ? inr[0] : inr[1])
+        continue;
       double *fld = (f < 4 ? NB + f * FP : DT + (2 + (f - 4)) * FP) + FK * r;
       double x[K], y[K];
 #pragma unroll
@@ -512,6 +603,20 @@ __device__ __forceinline__ void pr_face_axis(const ApplyParams<double> &prm, dou
                   g[e] = -(own_u[s][e] * jxw[s][e]);
                 }
             }
+          else if (inr[s])
+            {
+              const double2 nu = lds2(PNB[s] + (2 * (1 - s)) * FP + fp);
+              const double2 dn = lds2(PNB[s] + (2 * (1 - s) + 1) * FP + fp);
+              const double nuv[2] = {nu.x, nu.y}, dnv[2] = {dn.x, dn.y};
+              const double sgn = side == 0 ? 1.0 : -1.0;
+#pragma unroll
+              for (int e = 0; e < 2; ++e)
+                {
+                  const double delta = own_u[s][e] - nuv[e];
+                  rv[e] = (delta * tau[s] - sgn * ((dn_own[s][e] + dnv[e]) * 0.5)) * jxw[s][e];
+                  g[e] = -(sgn * delta * jxw[s][e] * 0.5);
+                }
+            }
           else
             {
               const double2 nu = lds2(NB + (2 * s) * FP + fp), nw = lds2(NB + (2 * s + 1) * FP + fp);
@@ -543,6 +648,7 @@ __device__ __forceinline__ void pr_face_axis(const ApplyParams<double> &prm, dou
              g[1] * jo[s][1][td < A ? td : td + 1]);
     }
   __syncthreads();
+  before_wpass();
   // w = rv + Dco_t0^T rg_t0 (rows) ...
   for (int tk = t; tk < 2 * K; tk += L::G)
     {
@@ -594,10 +700,7 @@ __device__ __forceinline__ void pr_face_axis(const ApplyParams<double> &prm, dou
 }
 
 template <int K, bool COMPRESSED, int BASIS>
-#ifndef DGX_PAIRS_MINB
-#define DGX_PAIRS_MINB 3
-#endif
-__global__ void __launch_bounds__(PL<K>::THREADS, DGX_PAIRS_MINB)
+__global__ void __launch_bounds__(PL<K>::THREADS, PL<K>::MINB)
   sipg_pairs_kernel(const ApplyParams<double> prm)
 {
   constexpr bool HERM = BASIS == 2;
@@ -632,6 +735,8 @@ __global__ void __launch_bounds__(PL<K>::THREADS, DGX_PAIRS_MINB)
 
   const int slot = active ? prm.task_slot[task] : 0;
   const int geo = active ? prm.task_geo[task] : -1;
+  if (!active && t == 0)
+    reinterpret_cast<int *>(cell + L::OFF_TF)[12] = -3; // no brick partner here
 
   // task metadata of the CTAs one and two generations ahead (prm.ahead =
   // tasks resident on the device): the first link of their prologue's
@@ -667,6 +772,8 @@ __global__ void __launch_bounds__(PL<K>::THREADS, DGX_PAIRS_MINB)
         }
       for (int i = t; i < 6; i += GS)
         reinterpret_cast<int2 *>(cell + L::OFF_TF)[i] = prm.task_face[task * 6 + i];
+      if (t == 0)
+        reinterpret_cast<int *>(cell + L::OFF_TF)[12] = slot;
 #pragma unroll
       for (int phi = 0; phi < 6; ++phi)
         {
@@ -755,6 +862,28 @@ __global__ void __launch_bounds__(PL<K>::THREADS, DGX_PAIRS_MINB)
   }
   __syncthreads();
 
+  // cell record of the quadrature-point operation: its first point layers
+  // are loaded before the last face axis's test-side passes, so their latency
+  // overlaps face work
+  const bool sym = prm.sym != 0;
+  const int ncg = sym ? 6 : 10;
+  const double *cgb = prm.cell_geo + (long long)(geo >= 0 ? geo : 0) * ncg * (COMPRESSED ? 1 : NQ);
+#ifndef DGX_PAIRS_QDEPTH
+#define DGX_PAIRS_QDEPTH 2
+#endif
+  constexpr int QD = DGX_PAIRS_QDEPTH; // layers in flight
+  double2 gn[QD][10];
+  auto load_layer = [&](int m) {
+    if constexpr (!COMPRESSED)
+      {
+        const double *cg = cgb + 2 * c + K * w + K * K * m;
+#pragma unroll
+        for (int i = 0; i < 10; ++i)
+          gn[m % QD][i] = (geo >= 0 && i < ncg) ? __ldcs(reinterpret_cast<const double2 *>(cg + i * NQ))
+                                                : make_double2(0.0, 0.0);
+      }
+  };
+
   // ---- faces ------------------------------------------------------------
   {
     // tangential weight prod_t w[q_t] of the two face points (compressed)
@@ -775,9 +904,14 @@ __global__ void __launch_bounds__(PL<K>::THREADS, DGX_PAIRS_MINB)
             wf[e] = (1.0 * wa) * wb;
           }
       }
-    pr_face_axis<K, 0, COMPRESSED, HERM>(prm, cell, active, c, w, t, wf, sp);
-    pr_face_axis<K, 1, COMPRESSED, HERM>(prm, cell, active, c, w, t, wf, sp);
-    pr_face_axis<K, 2, COMPRESSED, HERM>(prm, cell, active, c, w, t, wf, sp);
+    auto none = [] {};
+    pr_face_axis<K, 0, COMPRESSED, HERM>(prm, cell, active, c, w, t, lc, wf, sp, none);
+    pr_face_axis<K, 1, COMPRESSED, HERM>(prm, cell, active, c, w, t, lc, wf, sp, none);
+    pr_face_axis<K, 2, COMPRESSED, HERM>(prm, cell, active, c, w, t, lc, wf, sp, [&] {
+#pragma unroll
+      for (int m = 0; m < QD - 1; ++m)
+        load_layer(m);
+    });
   }
 
   // ---- quadrature-point operation (operators.cpp:669-733), z-pencil pairs;
@@ -800,27 +934,6 @@ __global__ void __launch_bounds__(PL<K>::THREADS, DGX_PAIRS_MINB)
             wxy[e] = (1.0 * wa) * wb;
           }
       }
-    const bool sym = prm.sym != 0;
-    const int ncg = sym ? 6 : 10;
-    const double *cgb = prm.cell_geo + (long long)(geo >= 0 ? geo : 0) * ncg * (COMPRESSED ? 1 : NQ);
-#ifndef DGX_PAIRS_QDEPTH
-#define DGX_PAIRS_QDEPTH 2
-#endif
-    constexpr int QD = DGX_PAIRS_QDEPTH; // layers in flight
-    double2 gn[QD][10];
-    auto load_layer = [&](int m) {
-      if constexpr (!COMPRESSED)
-        {
-          const double *cg = cgb + 2 * c + K * w + K * K * m;
-#pragma unroll
-          for (int i = 0; i < 10; ++i)
-            gn[m % QD][i] = (geo >= 0 && i < ncg) ? __ldcs(reinterpret_cast<const double2 *>(cg + i * NQ))
-                                                  : make_double2(0.0, 0.0);
-        }
-    };
-#pragma unroll
-    for (int m = 0; m < QD - 1; ++m)
-      load_layer(m);
 #pragma unroll
     for (int m = 0; m < K; ++m)
       {

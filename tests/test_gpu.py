@@ -212,6 +212,12 @@ RANDOM = [
     (2, [7, 5], 7, False, ("vertex", 0.1), True, 3),
     (3, [2, 2, 2], 10, False, ("vertex", 0.1), False, 1),
     (3, [1, 1, 3], 3, True, None, False, 1),
+    # x-rows inside one CTA of the pencil-pair kernel (even k): faces between
+    # consecutive tasks take the partner's trace from shared memory
+    (3, [5, 2, 2], 5, True, ("reference", 0.04, 2), False, 1),
+    (3, [2, 3, 3], 3, True, None, False, 1),
+    (3, [6, 2, 2], 7, False, ("vertex", 0.1), True, 2),
+    (3, [7, 2, 1], 9, True, ("reference", 0.04, 2), False, 1),
 ]
 
 
@@ -239,6 +245,7 @@ RANDOM_BASES = [
     (3, [3, 4, 3], 4, True, None, False, 4, "hermite_like"),
     (2, [7, 5], 6, False, ("vertex", 0.1), False, 3, "hermite_like"),
     (3, [3, 3, 3], 8, False, ("reference", 0.05, 2), False, 2, "hermite_like"),
+    (3, [5, 3, 2], 5, True, ("reference", 0.04, 2), False, 1, "hermite_like"),
     (3, [3, 3, 2], 2, False, ("reference", 0.04, 2), False, 2, "lagrange_gauss"),
     (3, [3, 2, 2], 5, True, None, False, 1, "lagrange_gauss"),
     (2, [5, 4], 7, False, ("vertex", 0.1), True, 3, "lagrange_gauss"),

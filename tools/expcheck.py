@@ -18,6 +18,11 @@ cfgs = [
     (3, [4, 3, 3], p, True, None, False, 3),
     (3, [3, 3, 2], p, False, ("reference", 0.04, 2), False, 2, "hermite_like"),
     (3, [3, 2, 2], p, True, ("vertex", 0.1), False, 1, "lagrange_gauss"),
+    # brick-aligned meshes (every face of a brick CTA internal or external)
+    (3, [4, 4, 4], p, True, ("reference", 0.04, 2), False, 1),
+    (3, [4, 4, 2], p, False, ("vertex", 0.1), True, 2),
+    (3, [2, 2, 2], p, True, None, False, 1),
+    (3, [4, 2, 4], p, False, ("reference", 0.04, 2), False, 1, "hermite_like"),
 ]
 bad = 0
 for c in cfgs:
