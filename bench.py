@@ -350,16 +350,30 @@ def main():
     if not args.no_e2e:
         h2d = lay.total_size * esize if ws == 1 else lay.owned_size * esize
         d2h = lay.owned_size * esize
-        barrier()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        for _ in range(args.steps):
-            u[: h2d // esize].copy_(u_host[: h2d // esize], non_blocking=True)
-            step()
-            y_host[: d2h // esize].copy_(y[: d2h // esize], non_blocking=True)
-        e1.record(stream)
-        barrier()
-        te = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=f"cuda:{local}")
+        if ws == 1 and prec == "fp64":
+            # the public host-buffer call (dgx_apply_host: z-slab pipeline of
+            # H2D / apply / D2H on three streams); blocking, so it is timed
+            # by the host clock around synchronized calls
+            op.apply_host(u_host, y_host)  # first call builds the pipeline state
+            torch.cuda.synchronize()
+            barrier()
+            w0 = time.perf_counter()
+            for _ in range(args.steps):
+                op.apply_host(u_host, y_host)
+            torch.cuda.synchronize()
+            te = torch.tensor([(time.perf_counter() - w0) * 1e3], dtype=torch.float64,
+                              device=f"cuda:{local}")
+        else:
+            barrier()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            for _ in range(args.steps):
+                u[: h2d // esize].copy_(u_host[: h2d // esize], non_blocking=True)
+                step()
+                y_host[: d2h // esize].copy_(y[: d2h // esize], non_blocking=True)
+            e1.record(stream)
+            barrier()
+            te = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=f"cuda:{local}")
         if ws > 1:
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
         e2e = {"value": n_dofs / (float(te.item()) / args.steps * 1e-3), "unit": "DoF/s",

@@ -226,18 +226,7 @@ dgx_status dgx_apply_f32(dgx_op *op, float *u, float *y, const dgx_hooks *hooks,
 dgx_status dgx_apply_host(dgx_op *op, const double *u, double *y)
 {
   return guard([&] {
-    dgx::Operator &o = op_of(op);
-    if (o.precision() != 0)
-      dgx::fail(dgx::Code::invalid_argument, "dgx_apply_host: fp64 operators only");
-    dgx::cuda_check(cudaSetDevice(o.device()), "cudaSetDevice");
-    const long long n = o.layout().total_size();
-    dgx::DeviceArray<double> du(n), dy(n);
-    dgx::cuda_check(cudaMemcpy(du.get(), u, n * 8, cudaMemcpyHostToDevice), "h2d");
-    // ghosted layouts: the caller has completed the ghost update on the host
-    // side; run both phases and return the ghost contributions in y
-    o.apply_phase(1, du.get(), dy.get(), nullptr, false);
-    o.apply_phase(2, du.get(), dy.get(), nullptr, false);
-    dgx::cuda_check(cudaMemcpy(y, dy.get(), n * 8, cudaMemcpyDeviceToHost), "d2h");
+    op_of(op).apply_host(u, y);
   });
 }
 

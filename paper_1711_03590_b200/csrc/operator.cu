@@ -1,10 +1,12 @@
 // Rank operator: setup (layout, cell tasks, device geometry) and apply.
 // Mirrors RankOperator / OperatorImpl (reference operators.cpp:89-264).
 #include "operator.hpp"
+
 #include "sipg_params.hpp"
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 
 namespace dgx
@@ -585,6 +587,14 @@ void Operator::set_velocity(const double *c_cells, const double *c_faces, cudaSt
 template <typename Real>
 void Operator::launch_range(int begin, int count, const Real *u, Real *y, cudaStream_t s)
 {
+  launch_tasks(task_slot_.get() + begin, task_geo_.get() + begin,
+               task_face_.get() + (long long)begin * 2 * d_, count, u, y, s);
+}
+
+template <typename Real>
+void Operator::launch_tasks(const int *tslot, const int *tgeo, const int2 *tface, int count,
+                            const Real *u, Real *y, cudaStream_t s)
+{
   if (count <= 0)
     return;
   if (kind_ == 1)
@@ -596,9 +606,9 @@ void Operator::launch_range(int begin, int count, const Real *u, Real *y, cudaSt
           ap.y = y;
           ap.cell = adv_cell_.get();
           ap.face = adv_face_.get();
-          ap.task_slot = task_slot_.get() + begin;
-          ap.task_geo = task_geo_.get() + begin;
-          ap.task_face = task_face_.get() + (long long)begin * 2 * d_;
+          ap.task_slot = tslot;
+          ap.task_geo = tgeo;
+          ap.task_face = tface;
           ap.n_tasks = count;
           ap.n_owned = static_cast<int>(layout_.n_owned);
           launch_adv(d_, k_, basis_, compressed_, ap, s);
@@ -622,9 +632,9 @@ void Operator::launch_range(int begin, int count, const Real *u, Real *y, cudaSt
       prm.face_geo = face_geo_f_.get();
       prm.penalty = penalty_f_.get();
     }
-  prm.task_slot = task_slot_.get() + begin;
-  prm.task_geo = task_geo_.get() + begin;
-  prm.task_face = task_face_.get() + (long long)begin * 2 * d_;
+  prm.task_slot = tslot;
+  prm.task_geo = tgeo;
+  prm.task_face = tface;
   prm.n_tasks = count;
   prm.n_owned = static_cast<int>(layout_.n_owned);
   prm.sym = sym_ ? 1 : 0;
@@ -682,6 +692,144 @@ void Operator::apply(void *u, void *y, const dgx_hooks *hooks, cudaStream_t s, b
     }
   if (hooks && hooks->compress)
     call(hooks->compress, y, "compress");
+}
+
+Operator::~Operator()
+{
+  if (pipe_.sh || pipe_.sc || pipe_.sd)
+    {
+      cudaSetDevice(device_);
+      for (cudaEvent_t e : pipe_.ev_h)
+        cudaEventDestroy(e);
+      for (cudaEvent_t e : pipe_.ev_c)
+        cudaEventDestroy(e);
+      cudaStreamDestroy(pipe_.sh);
+      cudaStreamDestroy(pipe_.sc);
+      cudaStreamDestroy(pipe_.sd);
+    }
+}
+
+// z-slab chunks of the owned cells (single rank: slot = global cell), task
+// lists reordered chunk by chunk (stable: the traversal order inside a chunk
+// is the apply's own)
+void Operator::build_host_pipe()
+{
+  HostPipe &P = pipe_;
+  P.built = true;
+  const long long n = layout_.total_size();
+  P.du.resize(n);
+  P.dy.resize(n);
+  P.pipelined = d_ == 3 && n_ranks_ == 1 && layout_.ghosts.empty() && n_coupled_ == 0 &&
+                precision_ == 0 && mesh_.cells[2] >= 4;
+  cuda_check(cudaStreamCreateWithFlags(&P.sh, cudaStreamNonBlocking), "cudaStreamCreate");
+  cuda_check(cudaStreamCreateWithFlags(&P.sc, cudaStreamNonBlocking), "cudaStreamCreate");
+  cuda_check(cudaStreamCreateWithFlags(&P.sd, cudaStreamNonBlocking), "cudaStreamCreate");
+  if (!P.pipelined)
+    return;
+  const int nz = mesh_.cells[2];
+  const long long layer = (long long)mesh_.cells[0] * mesh_.cells[1];
+  P.nchunk = std::min(64, nz / 2); // measured (C4 e2e): 16 / 32 / 64 slabs 5.51 / 5.80 / 5.84 GDoF/s
+  if (const char *e = std::getenv("DGX_HOST_CHUNKS"))
+    P.nchunk = std::max(2, std::min(nz, std::atoi(e)));
+  P.periodic_z = mesh_.periodic[2] != 0;
+  P.cell_begin.resize(P.nchunk + 1);
+  for (int k = 0; k <= P.nchunk; ++k)
+    P.cell_begin[k] = (long long)(nz * (long long)k / P.nchunk) * layer;
+  std::vector<std::vector<int>> idx(P.nchunk);
+  const int nt = n_inner_;
+  for (int i = 0; i < nt; ++i)
+    {
+      const long long c = host_task_slot_[i];
+      int k = (int)(c / layer * P.nchunk / nz);
+      while (k + 1 < P.nchunk && c >= P.cell_begin[k + 1])
+        ++k;
+      while (k > 0 && c < P.cell_begin[k])
+        --k;
+      idx[k].push_back(i);
+    }
+  std::vector<int> sl, ge;
+  std::vector<int2> fa;
+  P.task_begin.assign(1, 0);
+  for (int k = 0; k < P.nchunk; ++k)
+    {
+      for (int i : idx[k])
+        {
+          sl.push_back(host_task_slot_[i]);
+          ge.push_back(host_task_geo_[i]);
+          for (int f = 0; f < 2 * d_; ++f)
+            fa.push_back(host_task_face_[(size_t)i * 2 * d_ + f]);
+        }
+      P.task_begin.push_back((int)sl.size());
+    }
+  P.slot.upload(sl);
+  P.geo.upload(ge);
+  P.face.upload(fa);
+  P.ev_h.resize(P.nchunk);
+  P.ev_c.resize(P.nchunk);
+  for (int k = 0; k < P.nchunk; ++k)
+    {
+      cuda_check(cudaEventCreateWithFlags(&P.ev_h[k], cudaEventDisableTiming), "cudaEventCreate");
+      cuda_check(cudaEventCreateWithFlags(&P.ev_c[k], cudaEventDisableTiming), "cudaEventCreate");
+    }
+}
+
+void Operator::apply_host(const double *u, double *y)
+{
+  if (precision_ != 0)
+    fail(Code::invalid_argument, "dgx_apply_host: fp64 operators only");
+  if (host_only_)
+    fail(Code::invalid_argument, "apply: operator was created host-only (device < 0)");
+  cuda_check(cudaSetDevice(device_), "cudaSetDevice");
+  if (!pipe_.built)
+    build_host_pipe();
+  HostPipe &P = pipe_;
+  const long long n = layout_.total_size();
+  double *du = P.du.get(), *dy = P.dy.get();
+  if (!P.pipelined)
+    {
+      // ghosted layouts: the caller has completed the ghost update on the
+      // host side; both phases, y returns the ghost contributions
+      cuda_check(cudaMemcpyAsync(du, u, n * 8, cudaMemcpyHostToDevice, P.sc), "h2d");
+      apply_phase(1, du, dy, P.sc, false);
+      apply_phase(2, du, dy, P.sc, false);
+      cuda_check(cudaMemcpyAsync(y, dy, n * 8, cudaMemcpyDeviceToHost, P.sc), "d2h");
+      cuda_check(cudaStreamSynchronize(P.sc), "apply_host");
+      return;
+    }
+  const long long nq = nq_;
+  const int S = P.nchunk;
+  for (int k = 0; k < S; ++k)
+    {
+      const long long c0 = P.cell_begin[k], c1 = P.cell_begin[k + 1];
+      cuda_check(cudaMemcpyAsync(du + c0 * nq, u + c0 * nq, (c1 - c0) * nq * 8, cudaMemcpyHostToDevice,
+                                 P.sh),
+                 "h2d");
+      cuda_check(cudaEventRecord(P.ev_h[k], P.sh), "cudaEventRecord");
+    }
+  // a chunk reads its neighbours' u across z: wait for the H2D of the chunk
+  // above (in-order copies imply the ones below); with periodic z chunk 0
+  // also reads the last chunk, so it runs last
+  std::vector<int> order;
+  for (int k = P.periodic_z ? 1 : 0; k < S; ++k)
+    order.push_back(k);
+  if (P.periodic_z)
+    order.push_back(0);
+  for (int k : order)
+    {
+      const int need = P.periodic_z && k == 0 ? S - 1 : std::min(k + 1, S - 1);
+      cuda_check(cudaStreamWaitEvent(P.sc, P.ev_h[need], 0), "cudaStreamWaitEvent");
+      launch_tasks(P.slot.get() + P.task_begin[k], P.geo.get() + P.task_begin[k],
+                   P.face.get() + (long long)P.task_begin[k] * 2 * d_, P.task_begin[k + 1] - P.task_begin[k],
+                   du, dy, P.sc);
+      cuda_check(cudaEventRecord(P.ev_c[k], P.sc), "cudaEventRecord");
+      cuda_check(cudaStreamWaitEvent(P.sd, P.ev_c[k], 0), "cudaStreamWaitEvent");
+      const long long c0 = P.cell_begin[k], c1 = P.cell_begin[k + 1];
+      cuda_check(cudaMemcpyAsync(y + c0 * nq, dy + c0 * nq, (c1 - c0) * nq * 8, cudaMemcpyDeviceToHost,
+                                 P.sd),
+                 "d2h");
+    }
+  cuda_check(cudaStreamSynchronize(P.sd), "apply_host");
+  cuda_check(cudaStreamSynchronize(P.sc), "apply_host");
 }
 
 void Operator::accumulate_plan(int idx, const double *contrib, double *y, cudaStream_t s)

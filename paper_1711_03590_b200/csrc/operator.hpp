@@ -17,11 +17,18 @@ class Operator
 {
 public:
   Operator(const dgx_setup &s, int device);
+  ~Operator();
+  Operator(const Operator &) = delete;
+  Operator &operator=(const Operator &) = delete;
 
   void apply(void *u, void *y, const dgx_hooks *hooks, cudaStream_t stream, bool fp32);
   // phase 1: inner tasks; phase 2: ghost-coupled + ghost-side tasks
   void apply_phase(int phase, const void *u, void *y, cudaStream_t stream, bool fp32);
   void accumulate_plan(int idx, const double *contrib, double *y, cudaStream_t s);
+  // y = A u with host buffers (dgx_apply_host): single-rank 3D layouts run a
+  // z-slab pipeline (H2D of slab k+1, apply of slab k, D2H of slab k-1 on
+  // three streams); other layouts H2D, both phases, D2H. Blocking.
+  void apply_host(const double *u, double *y);
 
   const RankLayout &layout() const { return layout_; }
   int d() const { return d_; }
@@ -66,6 +73,24 @@ private:
   void build_geometry(const dgx_setup &s, const std::vector<RawFace> &faces);
   template <typename Real>
   void launch_range(int begin, int count, const Real *u, Real *y, cudaStream_t s);
+  template <typename Real>
+  void launch_tasks(const int *slot, const int *geo, const int2 *face, int count, const Real *u,
+                    Real *y, cudaStream_t s);
+
+  // host-buffer pipeline state (apply_host), built on first use
+  struct HostPipe
+  {
+    bool built = false, pipelined = false, periodic_z = false;
+    int nchunk = 0;
+    std::vector<int> task_begin;       // per chunk, into the chunk-ordered task arrays (+ end)
+    std::vector<long long> cell_begin; // per chunk, first owned cell (+ end)
+    DeviceArray<int> slot, geo;
+    DeviceArray<int2> face;
+    DeviceArray<double> du, dy;
+    cudaStream_t sh = nullptr, sc = nullptr, sd = nullptr;
+    std::vector<cudaEvent_t> ev_h, ev_c;
+  } pipe_;
+  void build_host_pipe();
 
   MeshDesc mesh_;
   int d_ = 3, p_ = 1, k_ = 2, precision_ = 0, device_ = 0, n_ranks_ = 1, basis_ = 0;

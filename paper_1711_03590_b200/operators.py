@@ -307,14 +307,25 @@ class RankOperator:
         check(lib().dgx_accumulate_plan(self._h, C.c_int(idx), _ptr(contrib),
                                         _ptr(y), _stream(stream)))
 
-    def apply_host(self, u: np.ndarray) -> np.ndarray:
-        """Host buffers in, host buffer out (H2D, apply, D2H)."""
-        u = np.ascontiguousarray(u, np.float64)
-        if u.size != self._layout.total_size:
+    def apply_host(self, u, y=None):
+        """Host buffers in, host buffer out (dgx_apply_host: single-rank 3D
+        layouts pipeline H2D / apply / D2H over z-slabs). u, y: numpy arrays
+        or CPU torch tensors (pinned memory lets the copies overlap the
+        apply); y is allocated when None. Returns y."""
+        def host_ptr(a):
+            if isinstance(a, np.ndarray):
+                return a.ctypes.data_as(C.c_void_p), a.size, a.dtype == np.float64
+            return C.c_void_p(a.data_ptr()), a.numel(), str(a.dtype) == "torch.float64"
+        if isinstance(u, np.ndarray):
+            u = np.ascontiguousarray(u, np.float64)
+        if y is None:
+            y = np.empty(self._layout.total_size) if isinstance(u, np.ndarray) else u.new_empty(u.shape)
+        (pu, nu, okd_u), (py, ny, okd_y) = host_ptr(u), host_ptr(y)
+        if nu != self._layout.total_size or ny != self._layout.total_size:
             raise _lib.DgxInvalidArgument("apply: vector size mismatch")
-        y = np.empty_like(u)
-        check(lib().dgx_apply_host(self._h, u.ctypes.data_as(C.c_void_p),
-                                   y.ctypes.data_as(C.c_void_p)))
+        if not (okd_u and okd_y):
+            raise _lib.DgxInvalidArgument("apply_host: float64 host buffers expected")
+        check(lib().dgx_apply_host(self._h, pu, py))
         return y
 
     def quadrature_points(self, which="cells"):
