@@ -55,7 +55,7 @@ int kernel_brick(int D, int K)
 #define DGX_BR(KK)                                                                         \
   if (D == 3 && K == KK)                                                                   \
     return dev::PL<KK>::BRICK;
-  DGX_BR(4) DGX_BR(6) DGX_BR(8) DGX_BR(10)
+  DGX_BR(2) DGX_BR(4) DGX_BR(6) DGX_BR(8) DGX_BR(10)
 #undef DGX_BR
   return 0;
 #endif

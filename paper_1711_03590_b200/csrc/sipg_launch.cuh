@@ -103,7 +103,10 @@ template <typename KERN>
 void set_smem_once(KERN kern, size_t smem, std::set<int> &configured);
 
 #ifndef DGX_PAIRS
-#define DGX_PAIRS 1 // 3D, even K, fp64: the pencil-pair kernel (sipg_pairs.cuh)
+#define DGX_PAIRS 1 // 3D fp64, even K: the pencil-pair kernel (sipg_pairs.cuh)
+#endif
+#ifndef DGX_PAIRS_ODD
+#define DGX_PAIRS_ODD 0 // odd K through the padded pair kernel: correct, measured slower (C3 15.7 vs 17.6, C5 19.0 vs 23.7 GDoF/s)
 #endif
 
 template <int K, bool C>
@@ -137,7 +140,7 @@ void launch_pairs(const dev::ApplyParams<double> &prm, cudaStream_t s)
 template <typename Real, int D, int K, bool C>
 void launch_one(const dev::ApplyParams<Real> &prm, cudaStream_t s)
 {
-  if constexpr (DGX_PAIRS && D == 3 && K % 2 == 0 && sizeof(Real) == 8)
+  if constexpr (DGX_PAIRS && D == 3 && sizeof(Real) == 8 && (K % 2 == 0 || DGX_PAIRS_ODD))
     {
       launch_pairs<K, C>(prm, s);
       return;

@@ -37,15 +37,20 @@ constexpr int pr_stride(int lo, int h) // smallest even s >= lo with (s/2) % 8 =
 template <int K>
 struct PL
 {
-  static constexpr int H = K / 2;
+  // odd K: shared rows padded to KP = K + 1 (the second pencil of the last
+  // pair is a dummy living in the padding: x = K for z/y pairs, y = K for
+  // x pairs, t0 = K on faces); global accesses are then 8-byte scalars
+  static constexpr bool ODD = (K & 1) != 0;
+  static constexpr int KP = K + (K & 1);
+  static constexpr int H = KP / 2;
   static constexpr int P2 = K * H;
   static constexpr int NQ = K * K * K;
-  static constexpr int S2 = pr_stride(K * K, H); // volume plane stride
+  static constexpr int S2 = pr_stride(KP * (ODD ? KP : K), H); // volume plane stride
   static constexpr int FS = S2 * K;              // volume field (even)
-  static constexpr int FK = K;                   // face row stride
+  static constexpr int FK = KP;                  // face row stride
   // face field stride: K = 6 dense (FP/2 = 2 mod 8: the row passes and the
   // f-fastest column passes below are conflict-free)
-  static constexpr int FP = K == 6 ? 36 : pr_stride(K * K, H);
+  static constexpr int FP = K == 6 ? 36 : pr_stride(KP * K, H);
   static constexpr int OFF_G = FS;
   static constexpr int OFF_OUT = 4 * FS;         // 3 axes x (w0, w1, rgn0, rgn1)
   static constexpr int OFF_NB = OFF_OUT + 12 * FP;
@@ -94,32 +99,45 @@ __device__ __forceinline__ void sts2(double *p, double a, double b)
 }
 
 // offset of element m of pencil e (e = 0, 1) of the pair (c, w) along axis A
-// in a volume array with plane stride PS (row stride K)
-template <int K, int A, int PS>
+// in a volume array with row stride RS and plane stride PS
+template <int K, int A, int RS, int PS>
 __device__ __forceinline__ int pr_el(int c, int w, int e, int m)
 {
   if constexpr (A == 2)
-    return 2 * c + e + K * w + PS * m;
+    return 2 * c + e + RS * w + PS * m;
   else if constexpr (A == 1)
-    return 2 * c + e + K * m + PS * w;
+    return 2 * c + e + RS * m + PS * w;
   else
-    return m + K * (2 * c + e) + PS * w;
+    return m + RS * (2 * c + e) + PS * w;
+}
+// shared (padded) and global (unpadded, K^3 per cell) offsets
+template <int K, int A>
+__device__ __forceinline__ int pr_sh(int c, int w, int e, int m)
+{
+  return pr_el<K, A, PL<K>::KP, PL<K>::S2>(c, w, e, m);
+}
+template <int K, int A>
+__device__ __forceinline__ int pr_gl(int c, int w, int e, int m)
+{
+  return pr_el<K, A, K, K * K>(c, w, e, m);
 }
 
-// load / store the pencil pair (c, w) along A: x[e][m]
-template <int K, int A, int PS>
+// load / store the pencil pair (c, w) along A in shared memory: x[e][m]
+template <int K, int A>
 __device__ __forceinline__ void pr_load(const double *f, int c, int w, double (&x)[2][K])
 {
+  constexpr int H = PL<K>::H;
   if constexpr (A == 0)
     {
 #pragma unroll
       for (int e = 0; e < 2; ++e)
 #pragma unroll
-        for (int j = 0; j < K / 2; ++j)
+        for (int j = 0; j < H; ++j)
           {
-            const double2 v = lds2(f + pr_el<K, A, PS>(c, w, e, 2 * j));
+            const double2 v = lds2(f + pr_sh<K, A>(c, w, e, 2 * j));
             x[e][2 * j] = v.x;
-            x[e][2 * j + 1] = v.y;
+            if (2 * j + 1 < K)
+              x[e][2 * j + 1] = v.y;
           }
     }
   else
@@ -127,87 +145,81 @@ __device__ __forceinline__ void pr_load(const double *f, int c, int w, double (&
 #pragma unroll
       for (int m = 0; m < K; ++m)
         {
-          const double2 v = lds2(f + pr_el<K, A, PS>(c, w, 0, m));
+          const double2 v = lds2(f + pr_sh<K, A>(c, w, 0, m));
           x[0][m] = v.x;
           x[1][m] = v.y;
         }
     }
 }
-template <int K, int A, int PS>
+template <int K, int A>
 __device__ __forceinline__ void pr_store(double *f, int c, int w, const double (&x)[2][K])
 {
+  constexpr int H = PL<K>::H;
   if constexpr (A == 0)
     {
 #pragma unroll
       for (int e = 0; e < 2; ++e)
 #pragma unroll
-        for (int j = 0; j < K / 2; ++j)
-          sts2(f + pr_el<K, A, PS>(c, w, e, 2 * j), x[e][2 * j], x[e][2 * j + 1]);
+        for (int j = 0; j < H; ++j)
+          sts2(f + pr_sh<K, A>(c, w, e, 2 * j), x[e][2 * j], 2 * j + 1 < K ? x[e][2 * j + 1] : 0.0);
     }
   else
     {
 #pragma unroll
       for (int m = 0; m < K; ++m)
-        sts2(f + pr_el<K, A, PS>(c, w, 0, m), x[0][m], x[1][m]);
-    }
-}
-// global (read-only path) variant
-template <int K, int A, int PS>
-__device__ __forceinline__ void pr_ldg(const double *f, int c, int w, double (&x)[2][K])
-{
-  if constexpr (A == 0)
-    {
-#pragma unroll
-      for (int e = 0; e < 2; ++e)
-#pragma unroll
-        for (int j = 0; j < K / 2; ++j)
-          {
-            const double2 v = __ldg(reinterpret_cast<const double2 *>(f + pr_el<K, A, PS>(c, w, e, 2 * j)));
-            x[e][2 * j] = v.x;
-            x[e][2 * j + 1] = v.y;
-          }
-    }
-  else
-    {
-#pragma unroll
-      for (int m = 0; m < K; ++m)
-        {
-          const double2 v = __ldg(reinterpret_cast<const double2 *>(f + pr_el<K, A, PS>(c, w, 0, m)));
-          x[0][m] = v.x;
-          x[1][m] = v.y;
-        }
+        sts2(f + pr_sh<K, A>(c, w, 0, m), x[0][m], x[1][m]);
     }
 }
 
-// predicated variant (branch-free: the loads of both faces stay in flight
-// together); zeros where !pred
-template <int K, int A, int PS>
+// global (read-only path), predicated (branch-free: the loads of both faces
+// stay in flight together); zeros where !pred and for the dummy pencil of
+// an odd K. Even K: 16-byte pair loads; odd K: 8-byte loads (the pairs are
+// not 16-byte aligned in the unpadded global layout)
+template <int K, int A>
 __device__ __forceinline__ void pr_ldg_if(bool pred, const double *f, int c, int w, double (&x)[2][K])
 {
   const double2 z = make_double2(0.0, 0.0);
-  if constexpr (A == 0)
+  if constexpr (!PL<K>::ODD)
     {
+      if constexpr (A == 0)
+        {
 #pragma unroll
-      for (int e = 0; e < 2; ++e)
+          for (int e = 0; e < 2; ++e)
 #pragma unroll
-        for (int j = 0; j < K / 2; ++j)
-          {
-            const double2 v =
-              pred ? __ldg(reinterpret_cast<const double2 *>(f + pr_el<K, A, PS>(c, w, e, 2 * j))) : z;
-            x[e][2 * j] = v.x;
-            x[e][2 * j + 1] = v.y;
-          }
+            for (int j = 0; j < K / 2; ++j)
+              {
+                const double2 v =
+                  pred ? __ldg(reinterpret_cast<const double2 *>(f + pr_gl<K, A>(c, w, e, 2 * j))) : z;
+                x[e][2 * j] = v.x;
+                x[e][2 * j + 1] = v.y;
+              }
+        }
+      else
+        {
+#pragma unroll
+          for (int m = 0; m < K; ++m)
+            {
+              const double2 v = pred ? __ldg(reinterpret_cast<const double2 *>(f + pr_gl<K, A>(c, w, 0, m))) : z;
+              x[0][m] = v.x;
+              x[1][m] = v.y;
+            }
+        }
     }
   else
     {
+      const bool p1 = pred && 2 * c + 1 < K;
 #pragma unroll
       for (int m = 0; m < K; ++m)
         {
-          const double2 v = pred ? __ldg(reinterpret_cast<const double2 *>(f + pr_el<K, A, PS>(c, w, 0, m))) : z;
-          x[0][m] = v.x;
-          x[1][m] = v.y;
+          x[0][m] = pred ? __ldg(f + pr_gl<K, A>(c, w, 0, m)) : 0.0;
+          x[1][m] = p1 ? __ldg(f + pr_gl<K, A>(c, w, 1, m)) : 0.0;
         }
     }
+}
+template <int K, int A>
+__device__ __forceinline__ void pr_ldg(const double *f, int c, int w, double (&x)[2][K])
+{
+  pr_ldg_if<K, A>(true, f, c, w, x);
 }
 
 // elements m and m+1 of both pencils of the pair along A (global)
@@ -215,26 +227,44 @@ template <int K, int A>
 __device__ __forceinline__ void pr_ldg_two(const double *f, int c, int w, int m, double (&lo)[2],
                                            double (&hi)[2])
 {
-  constexpr int PS = K * K;
-  if constexpr (A == 0)
+  if constexpr (PL<K>::ODD)
+    {
+      const bool p1 = 2 * c + 1 < K;
+      lo[0] = __ldg(f + pr_gl<K, A>(c, w, 0, m));
+      hi[0] = __ldg(f + pr_gl<K, A>(c, w, 0, m + 1));
+      lo[1] = p1 ? __ldg(f + pr_gl<K, A>(c, w, 1, m)) : 0.0;
+      hi[1] = p1 ? __ldg(f + pr_gl<K, A>(c, w, 1, m + 1)) : 0.0;
+    }
+  else if constexpr (A == 0)
     {
 #pragma unroll
       for (int e = 0; e < 2; ++e)
         {
-          const double2 v = __ldg(reinterpret_cast<const double2 *>(f + pr_el<K, A, PS>(c, w, e, m)));
+          const double2 v = __ldg(reinterpret_cast<const double2 *>(f + pr_gl<K, A>(c, w, e, m)));
           lo[e] = v.x;
           hi[e] = v.y;
         }
     }
   else
     {
-      const double2 a = __ldg(reinterpret_cast<const double2 *>(f + pr_el<K, A, PS>(c, w, 0, m)));
-      const double2 b = __ldg(reinterpret_cast<const double2 *>(f + pr_el<K, A, PS>(c, w, 0, m + 1)));
+      const double2 a = __ldg(reinterpret_cast<const double2 *>(f + pr_gl<K, A>(c, w, 0, m)));
+      const double2 b = __ldg(reinterpret_cast<const double2 *>(f + pr_gl<K, A>(c, w, 0, m + 1)));
       lo[0] = a.x;
       lo[1] = a.y;
       hi[0] = b.x;
       hi[1] = b.y;
     }
+}
+
+// two values at global offset o (pair element e = 0) and o + 1 (e = 1; the
+// dummy of an odd K reads nothing)
+template <int K, bool LDCS = false>
+__device__ __forceinline__ double2 pr_ldg_pt(const double *f, bool p1)
+{
+  if constexpr (!PL<K>::ODD)
+    return LDCS ? __ldcs(reinterpret_cast<const double2 *>(f)) : __ldg(reinterpret_cast<const double2 *>(f));
+  else
+    return make_double2(LDCS ? __ldcs(f) : __ldg(f), p1 ? (LDCS ? __ldcs(f + 1) : __ldg(f + 1)) : 0.0);
 }
 
 template <int K, int A>
@@ -302,7 +332,9 @@ __device__ __forceinline__ void pr_face_axis(const ApplyParams<double> &prm, dou
   double *NB = cell + L::OFF_NB;
   double *DT = cell + L::OFF_DT;
   double *OUT = cell + L::OFF_OUT + (2 * A) * 2 * FP;
-  const int fp = 2 * c + FK * w;
+  const int fp = 2 * c + FK * w;     // shared face fields
+  const int fpg = 2 * c + K * w;     // global face records (unpadded)
+  const bool p1 = 2 * c + 1 < K;     // second point of the pair real (odd K: last pair)
 
   int2 tf[2] = {make_int2(-2, 0), make_int2(-2, 0)};
   if (active)
@@ -383,7 +415,7 @@ __device__ __forceinline__ void pr_face_axis(const ApplyParams<double> &prm, dou
       for (int s = 0; s < 2; ++s)
         {
 #ifdef DGX_NBLOAD_OLD
-          pr_ldg<K, A, K * K>(prm.u + (long long)(tf[s].x >= 0 ? tf[s].x : 0) * NQ, c, w, x[s]);
+          pr_ldg<K, A>(prm.u + (long long)(tf[s].x >= 0 ? tf[s].x : 0) * NQ, c, w, x[s]);
           if (tf[s].x < 0)
 #pragma unroll
             for (int e = 0; e < 2; ++e)
@@ -391,7 +423,7 @@ __device__ __forceinline__ void pr_face_axis(const ApplyParams<double> &prm, dou
               for (int m = 0; m < K; ++m)
                 x[s][e][m] = 0.0;
 #else
-          pr_ldg_if<K, A, K * K>(tf[s].x >= 0 && !inr[s], prm.u + (long long)(tf[s].x >= 0 ? tf[s].x : 0) * NQ,
+          pr_ldg_if<K, A>(tf[s].x >= 0 && !inr[s], prm.u + (long long)(tf[s].x >= 0 ? tf[s].x : 0) * NQ,
                                  c, w, x[s]);
 #endif
         }
@@ -404,7 +436,7 @@ __device__ __forceinline__ void pr_face_axis(const ApplyParams<double> &prm, dou
   double own_u[2][2], own_g[2][2][3];
   {
     double x[2][K];
-    pr_load<K, A, S2>(val, c, w, x);
+    pr_load<K, A>(val, c, w, x);
 #pragma unroll
     for (int e = 0; e < 2; ++e)
       {
@@ -414,7 +446,7 @@ __device__ __forceinline__ void pr_face_axis(const ApplyParams<double> &prm, dou
 #pragma unroll
     for (int b = 0; b < 3; ++b)
       {
-        pr_load<K, A, S2>(G + b * FS, c, w, x);
+        pr_load<K, A>(G + b * FS, c, w, x);
 #pragma unroll
         for (int e = 0; e < 2; ++e)
           {
@@ -449,11 +481,11 @@ __device__ __forceinline__ void pr_face_axis(const ApplyParams<double> &prm, dou
             }
           else
             {
-              const double *fg = prm.face_geo + (long long)fid * 7 * P + fp;
+              const double *fg = prm.face_geo + (long long)fid * 7 * P + fpg;
 #pragma unroll
               for (int b = 0; b < 3; ++b)
                 {
-                  const double2 o = __ldg(reinterpret_cast<const double2 *>(fg + (1 + side * 3 + b) * P));
+                  const double2 o = pr_ldg_pt<K>(fg + (1 + side * 3 + b) * P, p1);
                   jo[s][0][b] = o.x;
                   jo[s][1][b] = o.y;
                 }
@@ -539,15 +571,14 @@ __device__ __forceinline__ void pr_face_axis(const ApplyParams<double> &prm, dou
             }
           else
             {
-              const double *fg = prm.face_geo + (long long)fid * 7 * P + fp;
-              const double2 j2 = __ldg(reinterpret_cast<const double2 *>(fg));
+              const double *fg = prm.face_geo + (long long)fid * 7 * P + fpg;
+              const double2 j2 = pr_ldg_pt<K>(fg, p1);
               jxw[s][0] = j2.x;
               jxw[s][1] = j2.y;
 #pragma unroll
-#pragma unroll
               for (int b = 0; b < 3; ++b)
                 {
-                  const double2 n = !inr[s] ? __ldg(reinterpret_cast<const double2 *>(fg + (1 + (1 - side) * 3 + b) * P))
+                  const double2 n = !inr[s] ? pr_ldg_pt<K>(fg + (1 + (1 - side) * 3 + b) * P, p1)
                                             : make_double2(0.0, 0.0);
                   jb[s][0][b] = n.x;
                   jb[s][1][b] = n.y;
@@ -569,19 +600,20 @@ __device__ __forceinline__ void pr_face_axis(const ApplyParams<double> &prm, dou
         {
           const double2 v = lds2(fld + 2 * j);
           x[2 * j] = v.x;
-          x[2 * j + 1] = v.y;
+          if (2 * j + 1 < K)
+            x[2 * j + 1] = v.y;
         }
       apply_S<double, K>(x, y);
 #pragma unroll
       for (int j = 0; j < H; ++j)
-        sts2(fld + 2 * j, y[2 * j], y[2 * j + 1]);
+        sts2(fld + 2 * j, y[2 * j], 2 * j + 1 < K ? y[2 * j + 1] : 0.0);
       if (f < 4 && (f & 1) == 0)
         {
           apply_Dn<double, K>(x, y);
           double *dt = DT + (f / 2) * FP + FK * r;
 #pragma unroll
           for (int j = 0; j < H; ++j)
-            sts2(dt + 2 * j, y[2 * j], y[2 * j + 1]);
+            sts2(dt + 2 * j, y[2 * j], 2 * j + 1 < K ? y[2 * j + 1] : 0.0);
         }
     }
   __syncthreads();
@@ -661,14 +693,17 @@ __device__ __forceinline__ void pr_face_axis(const ApplyParams<double> &prm, dou
         {
           const double2 v = lds2(xo + 2 * j), u = lds2(yo + 2 * j);
           a[2 * j] = v.x;
-          a[2 * j + 1] = v.y;
           y[2 * j] = u.x;
-          y[2 * j + 1] = u.y;
+          if (2 * j + 1 < K)
+            {
+              a[2 * j + 1] = v.y;
+              y[2 * j + 1] = u.y;
+            }
         }
       apply_Dt<double, K>(y, b);
 #pragma unroll
       for (int j = 0; j < H; ++j)
-        sts2(xo + 2 * j, a[2 * j] + b[2 * j], a[2 * j + 1] + b[2 * j + 1]);
+        sts2(xo + 2 * j, a[2 * j] + b[2 * j], 2 * j + 1 < K ? a[2 * j + 1] + b[2 * j + 1] : 0.0);
     }
   __syncthreads();
   // ... + Dco_t1^T rg_t1 (column pairs)
@@ -815,7 +850,7 @@ __global__ void __launch_bounds__(PL<K>::THREADS, PL<K>::MINB)
     double x[2][K], z[2][K];
     const double *uc = prm.u + (long long)slot * NQ;
     if (active)
-      pr_ldg<K, 2, K * K>(uc, c, w, x);
+      pr_ldg<K, 2>(uc, c, w, x);
     else
 #pragma unroll
       for (int e = 0; e < 2; ++e)
@@ -831,34 +866,34 @@ __global__ void __launch_bounds__(PL<K>::THREADS, PL<K>::MINB)
 #pragma unroll
     for (int e = 0; e < 2; ++e)
       apply_S<double, K>(x[e], z[e]);
-    pr_store<K, 2, S2>(val, c, w, z);
+    pr_store<K, 2>(val, c, w, z);
     __syncthreads();
-    pr_load<K, 0, S2>(val, cx, wx, x);
+    pr_load<K, 0>(val, cx, wx, x);
 #pragma unroll
     for (int e = 0; e < 2; ++e)
       apply_S<double, K>(x[e], z[e]);
-    pr_store<K, 0, S2>(val, cx, wx, z);
+    pr_store<K, 0>(val, cx, wx, z);
     __syncthreads();
-    pr_load<K, 1, S2>(val, c, w, x);
+    pr_load<K, 1>(val, c, w, x);
 #pragma unroll
     for (int e = 0; e < 2; ++e)
       apply_S<double, K>(x[e], z[e]);
-    pr_store<K, 1, S2>(val, c, w, z);
+    pr_store<K, 1>(val, c, w, z);
 #pragma unroll
     for (int e = 0; e < 2; ++e)
       apply_D<double, K>(z[e], x[e]);
-    pr_store<K, 1, S2>(G + FS, c, w, x);
+    pr_store<K, 1>(G + FS, c, w, x);
     __syncthreads();
-    pr_load<K, 0, S2>(val, cx, wx, x);
+    pr_load<K, 0>(val, cx, wx, x);
 #pragma unroll
     for (int e = 0; e < 2; ++e)
       apply_D<double, K>(x[e], z[e]);
-    pr_store<K, 0, S2>(G, cx, wx, z);
-    pr_load<K, 2, S2>(val, c, w, x);
+    pr_store<K, 0>(G, cx, wx, z);
+    pr_load<K, 2>(val, c, w, x);
 #pragma unroll
     for (int e = 0; e < 2; ++e)
       apply_D<double, K>(x[e], z[e]);
-    pr_store<K, 2, S2>(G + 2 * FS, c, w, z);
+    pr_store<K, 2>(G + 2 * FS, c, w, z);
   }
   __syncthreads();
 
@@ -879,7 +914,7 @@ __global__ void __launch_bounds__(PL<K>::THREADS, PL<K>::MINB)
         const double *cg = cgb + 2 * c + K * w + K * K * m;
 #pragma unroll
         for (int i = 0; i < 10; ++i)
-          gn[m % QD][i] = (geo >= 0 && i < ncg) ? __ldcs(reinterpret_cast<const double2 *>(cg + i * NQ))
+          gn[m % QD][i] = (geo >= 0 && i < ncg) ? pr_ldg_pt<K, true>(cg + i * NQ, 2 * c + 1 < K)
                                                 : make_double2(0.0, 0.0);
       }
   };
@@ -937,7 +972,7 @@ __global__ void __launch_bounds__(PL<K>::THREADS, PL<K>::MINB)
 #pragma unroll
     for (int m = 0; m < K; ++m)
       {
-        const int q = 2 * c + K * w + S2 * m; // shared
+        const int q = 2 * c + L::KP * w + S2 * m; // shared
         if (m + QD - 1 < K)
           load_layer(m + QD - 1);
         double2 gc[10];
@@ -1037,31 +1072,31 @@ __global__ void __launch_bounds__(PL<K>::THREADS, PL<K>::MINB)
   // ---- backward: y = (S^T x S^T x S^T)(sum_b Dco_b^T t_b + face terms) ----
   {
     double x[2][K], z[2][K], v[2][K];
-    pr_load<K, 2, S2>(G + 2 * FS, c, w, x);
+    pr_load<K, 2>(G + 2 * FS, c, w, x);
 #pragma unroll
     for (int e = 0; e < 2; ++e)
       apply_Dt<double, K>(x[e], v[e]);
     pr_face_terms<K, 2>(cell, c, w, v);
-    pr_store<K, 2, S2>(val, c, w, v);
+    pr_store<K, 2>(val, c, w, v);
     __syncthreads();
-    pr_load<K, 1, S2>(G + FS, c, w, x);
+    pr_load<K, 1>(G + FS, c, w, x);
 #pragma unroll
     for (int e = 0; e < 2; ++e)
       apply_Dt<double, K>(x[e], z[e]);
-    pr_load<K, 1, S2>(val, c, w, v);
+    pr_load<K, 1>(val, c, w, v);
 #pragma unroll
     for (int e = 0; e < 2; ++e)
 #pragma unroll
       for (int m = 0; m < K; ++m)
         v[e][m] += z[e][m];
     pr_face_terms<K, 1>(cell, c, w, v);
-    pr_store<K, 1, S2>(val, c, w, v);
+    pr_store<K, 1>(val, c, w, v);
     __syncthreads();
-    pr_load<K, 0, S2>(G, cx, wx, x);
+    pr_load<K, 0>(G, cx, wx, x);
 #pragma unroll
     for (int e = 0; e < 2; ++e)
       apply_Dt<double, K>(x[e], z[e]);
-    pr_load<K, 0, S2>(val, cx, wx, v);
+    pr_load<K, 0>(val, cx, wx, v);
 #pragma unroll
     for (int e = 0; e < 2; ++e)
 #pragma unroll
@@ -1071,15 +1106,15 @@ __global__ void __launch_bounds__(PL<K>::THREADS, PL<K>::MINB)
 #pragma unroll
     for (int e = 0; e < 2; ++e)
       apply_St<double, K>(v[e], z[e]);
-    pr_store<K, 0, S2>(val, cx, wx, z);
+    pr_store<K, 0>(val, cx, wx, z);
     __syncthreads();
-    pr_load<K, 1, S2>(val, c, w, x);
+    pr_load<K, 1>(val, c, w, x);
 #pragma unroll
     for (int e = 0; e < 2; ++e)
       apply_St<double, K>(x[e], z[e]);
-    pr_store<K, 1, S2>(val, c, w, z);
+    pr_store<K, 1>(val, c, w, z);
     __syncthreads();
-    pr_load<K, 2, S2>(val, c, w, x);
+    pr_load<K, 2>(val, c, w, x);
 #pragma unroll
     for (int e = 0; e < 2; ++e)
       apply_St<double, K>(x[e], z[e]);
@@ -1095,7 +1130,14 @@ __global__ void __launch_bounds__(PL<K>::THREADS, PL<K>::MINB)
                 a = ((gmask[0] >> m) & 1u) ? a * (sp[0] * hsign<double, K>(m)) : 0.0;
                 b = ((gmask[1] >> m) & 1u) ? b * (sp[1] * hsign<double, K>(m)) : 0.0;
               }
-            *reinterpret_cast<double2 *>(yc + pr_el<K, 2, K * K>(c, w, 0, m)) = make_double2(a, b);
+            if constexpr (L::ODD)
+              {
+                yc[pr_gl<K, 2>(c, w, 0, m)] = a;
+                if (2 * c + 1 < K)
+                  yc[pr_gl<K, 2>(c, w, 1, m)] = b;
+              }
+            else
+              *reinterpret_cast<double2 *>(yc + pr_gl<K, 2>(c, w, 0, m)) = make_double2(a, b);
           }
       }
   }
