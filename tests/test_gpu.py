@@ -387,6 +387,9 @@ def dot(a, b):
     ("C1", 3, 16, 3, True, "cart"),
     ("C3", 3, 64, 4, False, "vertex"),
     ("C2", 2, 256, 7, False, "cart"),
+    # BASELINE sizes of the bench configurations (pencil-pair kernel; C5 odd k)
+    ("C4", 3, 128, 5, False, "vertex_a"),
+    ("C5", 3, 160, 6, False, "cart"),
 ])
 def test_full_size_properties(torch, shape):
     """Properties that hold at any size: symmetry v.Au = u.Av, linearity,
@@ -394,7 +397,9 @@ def test_full_size_properties(torch, shape):
     the kernel of the SIP Laplacian; GL nodal coefficients of 1 are 1)."""
     name, d, n, p, periodic, kind = shape
     D = dgx()
-    geo = D.Geometry(source="vertex_bump", vertex_bump_eps=0.1) if kind == "vertex" else D.Geometry()
+    geo = (D.Geometry(source="vertex_bump", vertex_bump_eps=0.1,
+                      coefficient="a1" if kind == "vertex_a" else None)
+           if kind.startswith("vertex") else D.Geometry())
     op = big_problem(torch, d, n, p, periodic, geo)
     N = op.layout().total_size
     g = torch.Generator(device="cuda").manual_seed(5)
