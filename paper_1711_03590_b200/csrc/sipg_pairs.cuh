@@ -940,6 +940,15 @@ __global__ void __launch_bounds__(PL<K>::THREADS, PL<K>::MINB)
           }
       }
     auto none = [] {};
+#ifdef DGX_EXP_PAIRS_NO_FACE // ablation: cell integral only
+    for (int i = t; i < 12 * L::FP; i += L::G)
+      cell[L::OFF_OUT + i] = 0.0;
+    __syncthreads();
+    (void)none;
+    (void)wf;
+    if (false)
+#endif
+    {
     pr_face_axis<K, 0, COMPRESSED, HERM>(prm, cell, active, c, w, t, lc, wf, sp, none);
     pr_face_axis<K, 1, COMPRESSED, HERM>(prm, cell, active, c, w, t, lc, wf, sp, none);
     pr_face_axis<K, 2, COMPRESSED, HERM>(prm, cell, active, c, w, t, lc, wf, sp, [&] {
@@ -947,6 +956,12 @@ __global__ void __launch_bounds__(PL<K>::THREADS, PL<K>::MINB)
       for (int m = 0; m < QD - 1; ++m)
         load_layer(m);
     });
+    }
+#ifdef DGX_EXP_PAIRS_NO_FACE
+#pragma unroll
+    for (int m = 0; m < QD - 1; ++m)
+      load_layer(m);
+#endif
   }
 
   // ---- quadrature-point operation (operators.cpp:669-733), z-pencil pairs;
