@@ -24,6 +24,12 @@
 // t_global + const across the cells of a CTA.
 #pragma once
 
+// One warp per cell (DGX_PAIRS_WARP): a cell's threads are one warp, so every
+// synchronisation is a __syncwarp and the cells of a CTA run independently
+#ifndef DGX_PAIRS_WARP
+#define DGX_PAIRS_WARP 0
+#endif
+
 namespace dgx
 {
 namespace dev
@@ -59,7 +65,10 @@ struct PL
   // threads per cell: P2 (option: rounded up to whole quarter-warps, so that
   // no quarter-warp mixes two cells; lanes >= P2 duplicate the last pair and
   // take line-operation tasks)
-#ifdef DGX_PAIRS_PAD // measured (C4): conflicts halve but the duplicated lanes cost more
+  static constexpr bool WARP = DGX_PAIRS_WARP && P2 <= 32;
+#if DGX_PAIRS_WARP
+  static constexpr int G = WARP ? 32 : P2;
+#elif defined(DGX_PAIRS_PAD) // measured (C4): conflicts halve but the duplicated lanes cost more
   static constexpr int G = (P2 + 7) / 8 * 8;
 #else
   static constexpr int G = P2;
@@ -76,8 +85,12 @@ struct PL
 #endif
   // BRICK 1: no reordering; consecutive tasks of the CTA that are
   // x-neighbours (the tiled task order runs along x) share their x-face.
+#if DGX_PAIRS_WARP
+  static constexpr int BRICK = 0; // cells do not synchronise with each other
+#else
   static constexpr int BRICK = (DGX_PAIRS_BRICK == 1 || (DGX_PAIRS_BRICK > 1 && DGX_PAIRS_BRICK * SM_CELL * 8 <= 113 * 1024))
                                  ? DGX_PAIRS_BRICK : 0;
+#endif
 #ifdef DGX_PAIRS_NC
   static constexpr int NC = DGX_PAIRS_NC;
 #else
@@ -91,6 +104,15 @@ struct PL
 #endif
   static constexpr int SMEM_REALS = NC * SM_CELL;
 };
+
+template <int K>
+__device__ __forceinline__ void pr_sync()
+{
+  if constexpr (PL<K>::WARP)
+    __syncwarp();
+  else
+    __syncthreads();
+}
 
 __device__ __forceinline__ double2 lds2(const double *p) { return *reinterpret_cast<const double2 *>(p); }
 __device__ __forceinline__ void sts2(double *p, double a, double b)
@@ -502,7 +524,7 @@ __device__ __forceinline__ void pr_face_axis(const ApplyParams<double> &prm, dou
           sts2(NB + (2 * s + 1) * FP + fp, dn_own[s][0], dn_own[s][1]);
         }
     }
-  __syncthreads();
+  pr_sync<K>();
 
   // pass 1, along t1 (column pairs): nu -> (S nu, D nu -> DT[2+s]); nw -> S nw
   for (int tk = t; tk < 4 * H; tk += L::G)
@@ -536,7 +558,7 @@ __device__ __forceinline__ void pr_face_axis(const ApplyParams<double> &prm, dou
             sts2(dt + FK * m, y[0][m], y[1][m]);
         }
     }
-  __syncthreads();
+  pr_sync<K>();
   // rest of the face geometry (L2-resident: prefetched at task start;
   // issued here so that pass 2 overlaps the latency)
   double jxw[2][2], tau[2], jb[2][2][3];
@@ -616,7 +638,7 @@ __device__ __forceinline__ void pr_face_axis(const ApplyParams<double> &prm, dou
             sts2(dt + 2 * j, y[2 * j], 2 * j + 1 < K ? y[2 * j + 1] : 0.0);
         }
     }
-  __syncthreads();
+  pr_sync<K>();
 
   // flux at the two face points of both faces
 #pragma unroll
@@ -679,7 +701,7 @@ __device__ __forceinline__ void pr_face_axis(const ApplyParams<double> &prm, dou
         sts2(DT + (2 * td + s) * FP + fp, g[0] * jo[s][0][td < A ? td : td + 1],
              g[1] * jo[s][1][td < A ? td : td + 1]);
     }
-  __syncthreads();
+  pr_sync<K>();
   before_wpass();
   // w = rv + Dco_t0^T rg_t0 (rows) ...
   for (int tk = t; tk < 2 * K; tk += L::G)
@@ -705,7 +727,7 @@ __device__ __forceinline__ void pr_face_axis(const ApplyParams<double> &prm, dou
       for (int j = 0; j < H; ++j)
         sts2(xo + 2 * j, a[2 * j] + b[2 * j], 2 * j + 1 < K ? a[2 * j + 1] + b[2 * j + 1] : 0.0);
     }
-  __syncthreads();
+  pr_sync<K>();
   // ... + Dco_t1^T rg_t1 (column pairs)
   for (int tk = t; tk < 2 * H; tk += L::G)
     {
@@ -867,13 +889,13 @@ __global__ void __launch_bounds__(PL<K>::THREADS, PL<K>::MINB)
     for (int e = 0; e < 2; ++e)
       apply_S<double, K>(x[e], z[e]);
     pr_store<K, 2>(val, c, w, z);
-    __syncthreads();
+    pr_sync<K>();
     pr_load<K, 0>(val, cx, wx, x);
 #pragma unroll
     for (int e = 0; e < 2; ++e)
       apply_S<double, K>(x[e], z[e]);
     pr_store<K, 0>(val, cx, wx, z);
-    __syncthreads();
+    pr_sync<K>();
     pr_load<K, 1>(val, c, w, x);
 #pragma unroll
     for (int e = 0; e < 2; ++e)
@@ -883,7 +905,7 @@ __global__ void __launch_bounds__(PL<K>::THREADS, PL<K>::MINB)
     for (int e = 0; e < 2; ++e)
       apply_D<double, K>(z[e], x[e]);
     pr_store<K, 1>(G + FS, c, w, x);
-    __syncthreads();
+    pr_sync<K>();
     pr_load<K, 0>(val, cx, wx, x);
 #pragma unroll
     for (int e = 0; e < 2; ++e)
@@ -895,7 +917,7 @@ __global__ void __launch_bounds__(PL<K>::THREADS, PL<K>::MINB)
       apply_D<double, K>(x[e], z[e]);
     pr_store<K, 2>(G + 2 * FS, c, w, z);
   }
-  __syncthreads();
+  pr_sync<K>();
 
   // cell record of the quadrature-point operation: its first point layers
   // are loaded before the last face axis's test-side passes, so their latency
@@ -943,7 +965,7 @@ __global__ void __launch_bounds__(PL<K>::THREADS, PL<K>::MINB)
 #ifdef DGX_EXP_PAIRS_NO_FACE // ablation: cell integral only
     for (int i = t; i < 12 * L::FP; i += L::G)
       cell[L::OFF_OUT + i] = 0.0;
-    __syncthreads();
+    pr_sync<K>();
     (void)none;
     (void)wf;
     if (false)
@@ -1082,7 +1104,7 @@ __global__ void __launch_bounds__(PL<K>::THREADS, PL<K>::MINB)
           sts2(G + b * FS + q, tt[b][0], tt[b][1]);
       }
   }
-  __syncthreads();
+  pr_sync<K>();
 
   // ---- backward: y = (S^T x S^T x S^T)(sum_b Dco_b^T t_b + face terms) ----
   {
@@ -1093,7 +1115,7 @@ __global__ void __launch_bounds__(PL<K>::THREADS, PL<K>::MINB)
       apply_Dt<double, K>(x[e], v[e]);
     pr_face_terms<K, 2>(cell, c, w, v);
     pr_store<K, 2>(val, c, w, v);
-    __syncthreads();
+    pr_sync<K>();
     pr_load<K, 1>(G + FS, c, w, x);
 #pragma unroll
     for (int e = 0; e < 2; ++e)
@@ -1106,7 +1128,7 @@ __global__ void __launch_bounds__(PL<K>::THREADS, PL<K>::MINB)
         v[e][m] += z[e][m];
     pr_face_terms<K, 1>(cell, c, w, v);
     pr_store<K, 1>(val, c, w, v);
-    __syncthreads();
+    pr_sync<K>();
     pr_load<K, 0>(G, cx, wx, x);
 #pragma unroll
     for (int e = 0; e < 2; ++e)
@@ -1122,13 +1144,13 @@ __global__ void __launch_bounds__(PL<K>::THREADS, PL<K>::MINB)
     for (int e = 0; e < 2; ++e)
       apply_St<double, K>(v[e], z[e]);
     pr_store<K, 0>(val, cx, wx, z);
-    __syncthreads();
+    pr_sync<K>();
     pr_load<K, 1>(val, c, w, x);
 #pragma unroll
     for (int e = 0; e < 2; ++e)
       apply_St<double, K>(x[e], z[e]);
     pr_store<K, 1>(val, c, w, z);
-    __syncthreads();
+    pr_sync<K>();
     pr_load<K, 2>(val, c, w, x);
 #pragma unroll
     for (int e = 0; e < 2; ++e)
