@@ -329,6 +329,28 @@ def test_apply_host_pointers(torch):
     assert rel_linf(y, c.g["y4"]) < TOL64
 
 
+@pytest.mark.parametrize("periodic", [False, True])
+def test_apply_host_pipeline_advection(torch, periodic):
+    """The z-slab host pipeline runs the advection operator too (its
+    neighbour reads cross z like the Laplacian's): same result as the
+    device apply."""
+    D = dgx()
+    cells, p = [3, 2, 10], 4
+    mesh = D.make_box_mesh(3, cells, 0.05, periodic, 2)
+    faces = D.enumerate_faces(mesh)
+    part = D.partition_cells(mesh, 1)
+    D.assign_face_owners(mesh, faces, part)
+    op = D.RankOperator(mesh, part, faces, D.Geometry(source="mesh"),
+                        D.OperatorConfig(d=3, p=p, kind="advection", velocity=(0.3, -0.7, 1.1)), 0)
+    x = D.random_vector(op.layout().total_size, 11)
+    u = torch.tensor(x, device="cuda:0")
+    yd = torch.empty_like(u)
+    op.apply(u, yd)
+    torch.cuda.synchronize()
+    yh = op.apply_host(x)
+    assert rel_linf(yh, yd.cpu().numpy()) < 1e-14
+
+
 @pytest.mark.parametrize("periodic,p,cells", [(False, 3, [3, 2, 9]), (True, 5, [2, 3, 8]),
                                               (True, 4, [2, 2, 33])])
 def test_apply_host_pipeline(torch, periodic, p, cells):
