@@ -1006,6 +1006,12 @@ __global__ void __launch_bounds__(PL<K>::THREADS, PL<K>::MINB)
             wxy[e] = (1.0 * wa) * wb;
           }
       }
+#ifndef DGX_PAIRS_FUSEQ
+#define DGX_PAIRS_FUSEQ 1
+#endif
+    // t_2 of the thread's own z-pencil pair stays in registers: the first
+    // backward pass (along z, same pencils) follows without a barrier
+    double t2r[2][K];
 #pragma unroll
     for (int m = 0; m < K; ++m)
       {
@@ -1100,15 +1106,27 @@ __global__ void __launch_bounds__(PL<K>::THREADS, PL<K>::MINB)
               tt[b][0] = tt[b][1] = 0.0;
           }
 #pragma unroll
-        for (int b = 0; b < 3; ++b)
+        for (int b = 0; b < (DGX_PAIRS_FUSEQ ? 2 : 3); ++b)
           sts2(G + b * FS + q, tt[b][0], tt[b][1]);
+        t2r[0][m] = tt[2][0];
+        t2r[1][m] = tt[2][1];
       }
+#if DGX_PAIRS_FUSEQ
+    // ---- backward, first pass (z): v = Dco_z^T t_2 + z-face terms
+    double v[2][K];
+#pragma unroll
+    for (int e = 0; e < 2; ++e)
+      apply_Dt<double, K>(t2r[e], v[e]);
+    pr_face_terms<K, 2>(cell, c, w, v);
+    pr_store<K, 2>(val, c, w, v);
+#endif
   }
   pr_sync<K>();
 
   // ---- backward: y = (S^T x S^T x S^T)(sum_b Dco_b^T t_b + face terms) ----
   {
     double x[2][K], z[2][K], v[2][K];
+#if !DGX_PAIRS_FUSEQ
     pr_load<K, 2>(G + 2 * FS, c, w, x);
 #pragma unroll
     for (int e = 0; e < 2; ++e)
@@ -1116,6 +1134,7 @@ __global__ void __launch_bounds__(PL<K>::THREADS, PL<K>::MINB)
     pr_face_terms<K, 2>(cell, c, w, v);
     pr_store<K, 2>(val, c, w, v);
     pr_sync<K>();
+#endif
     pr_load<K, 1>(G + FS, c, w, x);
 #pragma unroll
     for (int e = 0; e < 2; ++e)
