@@ -59,10 +59,11 @@ struct TabLayout
   static constexpr int oRD = oW + K;         // (rf Dco)[2][K] = (Dco^T rf^T)
   static constexpr int oDnE = oRD + 2 * K;   // even-odd halves of the nodal D
   static constexpr int oDnO = oDnE + CE * CE;
-  static constexpr int size = oDnO + CE * CE;
+  static constexpr int oDn = oDnO + CE * CE; // plain nodal D, K x K (Gauss point, node)
+  static constexpr int size = oDn + K * K;
 };
 
-constexpr int tab_size(int K) { return 10 * ((K + 1) / 2) * ((K + 1) / 2) + 2 * K * K + 9 * K; }
+constexpr int tab_size(int K) { return 10 * ((K + 1) / 2) * ((K + 1) / 2) + 3 * K * K + 9 * K; }
 // offset of the table for K (K >= 2) inside the per-precision constant block
 constexpr int tab_offset(int K) { return K <= 2 ? 0 : tab_offset(K - 1) + tab_size(K - 1); }
 constexpr int kMaxK = 11;

@@ -93,6 +93,9 @@ std::vector<double> build_table(int K)
       }
   o += 2 * K;
   eo_halves(t.D, K, o, o + c2); // nodal derivative D (basis.cpp:277-278)
+  o += 2 * c2;
+  for (int i = 0; i < K * K; ++i) // and plainly (row-dot neighbour traces, sipg_pairs.cuh)
+    o[i] = t.D[i];
   return tab;
 }
 

@@ -29,6 +29,11 @@
 #ifndef DGX_PAIRS_WARP
 #define DGX_PAIRS_WARP 0
 #endif
+// neighbour trace along t0 as row dot products at the thread's own face
+// points, fused with the flux (no row pass, one barrier less per axis)
+#ifndef DGX_PAIRS_ROWDOT
+#define DGX_PAIRS_ROWDOT 0 // measured (C4): 21.43 vs 20.99 ms (divergent constant loads, 168 registers)
+#endif
 
 namespace dgx
 {
@@ -61,7 +66,8 @@ struct PL
   static constexpr int OFF_OUT = 4 * FS;         // 3 axes x (w0, w1, rgn0, rgn1)
   static constexpr int OFF_NB = OFF_OUT + 12 * FP;
   static constexpr int OFF_DT = OFF_NB + 4 * FP;
-  static constexpr int OFF_TF = OFF_DT + 4 * FP; // 6 int2 face entries
+  static constexpr int OFF_RG1 = OFF_DT + 4 * FP; // row-dot variant: rg along t1, 2 faces
+  static constexpr int OFF_TF = OFF_RG1 + (DGX_PAIRS_ROWDOT ? 2 * FP : 0); // 6 int2 face entries
   // threads per cell: P2 (option: rounded up to whole quarter-warps, so that
   // no quarter-warp mixes two cells; lanes >= P2 duplicate the last pair and
   // take line-operation tasks)
@@ -609,6 +615,7 @@ __device__ __forceinline__ void pr_face_axis(const ApplyParams<double> &prm, dou
           tau[s] = __ldg(prm.penalty + fid);
         }
     }
+#if !DGX_PAIRS_ROWDOT
   // pass 2, along t0 (rows): nu -> (S nu, D nu -> DT[s]); nw, dt1 -> S
   for (int tk = t; tk < 6 * K; tk += L::G)
     {
@@ -639,6 +646,7 @@ __device__ __forceinline__ void pr_face_axis(const ApplyParams<double> &prm, dou
         }
     }
   pr_sync<K>();
+#endif
 
   // flux at the two face points of both faces
 #pragma unroll
@@ -673,10 +681,55 @@ __device__ __forceinline__ void pr_face_axis(const ApplyParams<double> &prm, dou
             }
           else
             {
+#if DGX_PAIRS_ROWDOT
+              // rows w of the t1-interpolated fields (value, normal derivative,
+              // t1-derivative), contracted along t0 at the two points:
+              // u+ = S nu, d/dt0 u+ = D nu, nw+ = S nw, d/dt1 u+ = S dt1
+              double rnu[K], rnw[K], rd1[K];
+              {
+                const double *r0 = NB + (2 * s) * FP + FK * w, *r1 = NB + (2 * s + 1) * FP + FK * w;
+                const double *r2 = DT + (2 + s) * FP + FK * w;
+#pragma unroll
+                for (int j = 0; j < H; ++j)
+                  {
+                    const double2 a0 = lds2(r0 + 2 * j), a1 = lds2(r1 + 2 * j), a2 = lds2(r2 + 2 * j);
+                    rnu[2 * j] = a0.x;
+                    rnw[2 * j] = a1.x;
+                    rd1[2 * j] = a2.x;
+                    if (2 * j + 1 < K)
+                      {
+                        rnu[2 * j + 1] = a0.y;
+                        rnw[2 * j + 1] = a1.y;
+                        rd1[2 * j + 1] = a2.y;
+                      }
+                  }
+              }
+              double nuv[2], nwv[2], dt0[2], dt1[2];
+#pragma unroll
+              for (int e = 0; e < 2; ++e)
+                {
+                  const int qr = (2 * c + e < K ? 2 * c + e : K - 1) * K;
+                  double a = 0.0, b = 0.0, cc = 0.0, dd = 0.0;
+#pragma unroll
+                  for (int j = 0; j < K; ++j)
+                    {
+                      const double sj = tab<double, K>(T::oS + qr + j), dj = tab<double, K>(T::oDn + qr + j);
+                      a += sj * rnu[j];
+                      b += dj * rnu[j];
+                      cc += sj * rnw[j];
+                      dd += sj * rd1[j];
+                    }
+                  nuv[e] = a;
+                  dt0[e] = b;
+                  nwv[e] = cc;
+                  dt1[e] = dd;
+                }
+#else
               const double2 nu = lds2(NB + (2 * s) * FP + fp), nw = lds2(NB + (2 * s + 1) * FP + fp);
               const double2 d0 = lds2(DT + s * FP + fp), d1 = lds2(DT + (2 + s) * FP + fp);
               const double nuv[2] = {nu.x, nu.y}, nwv[2] = {nw.x, nw.y};
               const double dt0[2] = {d0.x, d0.y}, dt1[2] = {d1.x, d1.y};
+#endif
               const double sgn = side == 0 ? 1.0 : -1.0;
 #pragma unroll
               for (int e = 0; e < 2; ++e)
@@ -696,10 +749,11 @@ __device__ __forceinline__ void pr_face_axis(const ApplyParams<double> &prm, dou
         }
       sts2(OUT + s * FP + fp, rv[0], rv[1]);
       sts2(OUT + (2 + s) * FP + fp, g[0] * jo[s][0][A], g[1] * jo[s][1][A]);
-#pragma unroll
-      for (int td = 0; td < 2; ++td)
-        sts2(DT + (2 * td + s) * FP + fp, g[0] * jo[s][0][td < A ? td : td + 1],
-             g[1] * jo[s][1][td < A ? td : td + 1]);
+      // rg along t0 -> DT[s]; along t1 -> DT[2 + s] (row-dot: RG1[s], since
+      // DT[2 + s] rows are still being read by the other threads of the row)
+      sts2(DT + s * FP + fp, g[0] * jo[s][0][A == 0 ? 1 : 0], g[1] * jo[s][1][A == 0 ? 1 : 0]);
+      sts2((DGX_PAIRS_ROWDOT ? cell + L::OFF_RG1 + s * FP : DT + (2 + s) * FP) + fp,
+           g[0] * jo[s][0][A == 2 ? 1 : 2], g[1] * jo[s][1][A == 2 ? 1 : 2]);
     }
   pr_sync<K>();
   before_wpass();
@@ -733,7 +787,7 @@ __device__ __forceinline__ void pr_face_axis(const ApplyParams<double> &prm, dou
     {
       const int s = tk / H, a2 = tk - s * H;
       double *xo = OUT + s * FP + 2 * a2;
-      const double *yo = DT + (2 + s) * FP + 2 * a2;
+      const double *yo = (DGX_PAIRS_ROWDOT ? cell + L::OFF_RG1 + s * FP : DT + (2 + s) * FP) + 2 * a2;
       double a[2][K], y[2][K], b[2][K];
 #pragma unroll
       for (int m = 0; m < K; ++m)
