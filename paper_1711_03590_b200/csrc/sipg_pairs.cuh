@@ -343,38 +343,23 @@ __device__ __forceinline__ void pr_face_terms(const double *cell, int c, int w, 
     }
 }
 
-// Both faces of axis A (same algebra as face_axis_v4, sipg_faces.cuh, with
-// the pair mapping): own traces, neighbour trace, SIPG flux
-// (operators.cpp:977-1003 interior, 1069-1089 boundary), test side.
-template <int K, int A, bool COMPRESSED, bool HERM, typename HOOK>
-__device__ __forceinline__ void pr_face_axis(const ApplyParams<double> &prm, double *cell, bool active,
-                                             int c, int w, int t, int lc, const double (&wf)[2],
-                                             const double (&sp)[2], HOOK &&before_wpass)
+// Face entries of axis A from the stash, and which of the two faces is
+// shared with the CTA partner (x-rows, BRICK 1; bricks, BRICK 4 / 8); PNB:
+// the partner's NB fields.
+template <int K, int A>
+__device__ __forceinline__ void pr_axis_faces(const double *cell, bool active, int lc, int2 (&tf)[2],
+                                              bool (&inr)[2], const double *(&PNB)[2])
 {
   using L = PL<K>;
-  using T = TabLayout<K>;
-  constexpr int P = K * K, NQ = L::NQ, FP = L::FP, FK = L::FK, H = L::H, P2 = L::P2, FS = L::FS;
-  constexpr int S2 = L::S2;
-  const double *val = cell;
-  const double *G = cell + L::OFF_G;
-  double *NB = cell + L::OFF_NB;
-  double *DT = cell + L::OFF_DT;
-  double *OUT = cell + L::OFF_OUT + (2 * A) * 2 * FP;
-  const int fp = 2 * c + FK * w;     // shared face fields
-  const int fpg = 2 * c + K * w;     // global face records (unpadded)
-  const bool p1 = 2 * c + 1 < K;     // second point of the pair real (odd K: last pair)
-
-  int2 tf[2] = {make_int2(-2, 0), make_int2(-2, 0)};
+  tf[0] = tf[1] = make_int2(-2, 0);
   if (active)
     {
       const int2 *tfs = reinterpret_cast<const int2 *>(cell + L::OFF_TF);
       tf[0] = tfs[2 * A];
       tf[1] = tfs[2 * A + 1];
     }
-  // face shared with the brick partner along A (its own trace and normal
-  // derivative are in its NB slots of the opposite side after the barrier)
-  bool inr[2] = {false, false};
-  const double *PNB[2] = {NB, NB};
+  inr[0] = inr[1] = false;
+  PNB[0] = PNB[1] = cell + L::OFF_NB;
   if constexpr (L::BRICK == 8 || (L::BRICK == 4 && A < 2))
     {
       const int lp = lc ^ (1 << A);
@@ -399,6 +384,54 @@ __device__ __forceinline__ void pr_face_axis(const ApplyParams<double> &prm, dou
             }
         }
     }
+}
+
+// The neighbour pencils through the thread's two face points of axis A
+// (nodal bases): issued one phase early so that their latency overlaps the
+// previous phase (the forward pass's last barrier for axis 0, the test-side
+// passes of axis A-1 otherwise).
+template <int K, int A>
+__device__ __forceinline__ void pr_nb_fetch(const ApplyParams<double> &prm, const double *cell, bool active,
+                                            int c, int w, int lc, double (&x)[2][2][K])
+{
+  int2 tf[2];
+  bool inr[2];
+  const double *PNB[2];
+  pr_axis_faces<K, A>(cell, active, lc, tf, inr, PNB);
+#pragma unroll
+  for (int s = 0; s < 2; ++s)
+    pr_ldg_if<K, A>(tf[s].x >= 0 && !inr[s], prm.u + (long long)(tf[s].x >= 0 ? tf[s].x : 0) * PL<K>::NQ,
+                    c, w, x[s]);
+}
+
+// Both faces of axis A (same algebra as face_axis_v4, sipg_faces.cuh, with
+// the pair mapping): own traces, neighbour trace, SIPG flux
+// (operators.cpp:977-1003 interior, 1069-1089 boundary), test side.
+template <int K, int A, bool COMPRESSED, bool HERM, typename HOOK>
+__device__ __forceinline__ void pr_face_axis(const ApplyParams<double> &prm, double *cell, bool active,
+                                             int c, int w, int t, int lc, const double (&wf)[2],
+                                             const double (&sp)[2], const double (&xnb)[2][2][K],
+                                             HOOK &&before_wpass)
+{
+  using L = PL<K>;
+  using T = TabLayout<K>;
+  constexpr int P = K * K, NQ = L::NQ, FP = L::FP, FK = L::FK, H = L::H, FS = L::FS;
+  const double *val = cell;
+  const double *G = cell + L::OFF_G;
+  double *NB = cell + L::OFF_NB;
+  double *DT = cell + L::OFF_DT;
+  double *OUT = cell + L::OFF_OUT + (2 * A) * 2 * FP;
+  const int fp = 2 * c + FK * w;     // shared face fields
+  const int fpg = 2 * c + K * w;     // global face records (unpadded)
+  const bool p1 = 2 * c + 1 < K;     // second point of the pair real (odd K: last pair)
+
+  // face entries; faces shared with the CTA partner (its own trace and
+  // normal derivative are in its NB slots of the opposite side after the
+  // barrier)
+  int2 tf[2];
+  bool inr[2];
+  const double *PNB[2];
+  pr_axis_faces<K, A>(cell, active, lc, tf, inr, PNB);
   // neighbour nodal value / normal-derivative layers at the two points
   if constexpr (HERM)
     {
@@ -438,23 +471,7 @@ __device__ __forceinline__ void pr_face_axis(const ApplyParams<double> &prm, dou
     }
   else
     {
-      double x[2][2][K];
-#pragma unroll
-      for (int s = 0; s < 2; ++s)
-        {
-#ifdef DGX_NBLOAD_OLD
-          pr_ldg<K, A>(prm.u + (long long)(tf[s].x >= 0 ? tf[s].x : 0) * NQ, c, w, x[s]);
-          if (tf[s].x < 0)
-#pragma unroll
-            for (int e = 0; e < 2; ++e)
-#pragma unroll
-              for (int m = 0; m < K; ++m)
-                x[s][e][m] = 0.0;
-#else
-          pr_ldg_if<K, A>(tf[s].x >= 0 && !inr[s], prm.u + (long long)(tf[s].x >= 0 ? tf[s].x : 0) * NQ,
-                                 c, w, x[s]);
-#endif
-        }
+      const double(&x)[2][2][K] = xnb; // fetched one phase early (pr_nb_fetch)
       sts2(NB + fp, dot_row<double, K, T::oSf + K>(x[0][0]), dot_row<double, K, T::oSf + K>(x[0][1]));
       sts2(NB + FP + fp, dot_row<double, K, T::oDf + K>(x[0][0]), dot_row<double, K, T::oDf + K>(x[0][1]));
       sts2(NB + 2 * FP + fp, dot_row<double, K, T::oSf>(x[1][0]), dot_row<double, K, T::oSf>(x[1][1]));
@@ -971,6 +988,10 @@ __global__ void __launch_bounds__(PL<K>::THREADS, PL<K>::MINB)
       apply_D<double, K>(x[e], z[e]);
     pr_store<K, 2>(G + 2 * FS, c, w, z);
   }
+  // neighbour pencils of the first face axis, in flight across the barrier
+  double xnb[2][2][K];
+  if constexpr (!HERM)
+    pr_nb_fetch<K, 0>(prm, cell, active, c, w, lc, xnb);
   pr_sync<K>();
 
   // cell record of the quadrature-point operation: its first point layers
@@ -1022,12 +1043,19 @@ __global__ void __launch_bounds__(PL<K>::THREADS, PL<K>::MINB)
     pr_sync<K>();
     (void)none;
     (void)wf;
+    (void)xnb;
     if (false)
 #endif
     {
-    pr_face_axis<K, 0, COMPRESSED, HERM>(prm, cell, active, c, w, t, lc, wf, sp, none);
-    pr_face_axis<K, 1, COMPRESSED, HERM>(prm, cell, active, c, w, t, lc, wf, sp, none);
-    pr_face_axis<K, 2, COMPRESSED, HERM>(prm, cell, active, c, w, t, lc, wf, sp, [&] {
+    pr_face_axis<K, 0, COMPRESSED, HERM>(prm, cell, active, c, w, t, lc, wf, sp, xnb, [&] {
+      if constexpr (!HERM)
+        pr_nb_fetch<K, 1>(prm, cell, active, c, w, lc, xnb);
+    });
+    pr_face_axis<K, 1, COMPRESSED, HERM>(prm, cell, active, c, w, t, lc, wf, sp, xnb, [&] {
+      if constexpr (!HERM)
+        pr_nb_fetch<K, 2>(prm, cell, active, c, w, lc, xnb);
+    });
+    pr_face_axis<K, 2, COMPRESSED, HERM>(prm, cell, active, c, w, t, lc, wf, sp, xnb, [&] {
 #pragma unroll
       for (int m = 0; m < QD - 1; ++m)
         load_layer(m);
