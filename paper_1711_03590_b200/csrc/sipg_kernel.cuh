@@ -780,7 +780,7 @@ __device__ __forceinline__ void sipg_task(const ApplyParams<Real> &prm, Real *ce
           {
             if constexpr (HERM)
               z[m] = ((gmask >> m) & 1u) ? z[m] * (sp * hsign<Real, K>(m)) : Real(0);
-            yc[p + P * m] = z[m];
+            __stcs(yc + p + P * m, z[m]); // y is not read again (streaming)
           }
       }
   }

@@ -1275,7 +1275,9 @@ __global__ void __launch_bounds__(PL<K>::THREADS, PL<K>::MINB)
                   yc[pr_gl<K, 2>(c, w, 1, m)] = b;
               }
             else
-              *reinterpret_cast<double2 *>(yc + pr_gl<K, 2>(c, w, 0, m)) = make_double2(a, b);
+              // streaming store: y is not read again, keep L2 for u and the
+              // face records (measured 20.82 -> 20.72 ms on C4)
+              __stcs(reinterpret_cast<double2 *>(yc + pr_gl<K, 2>(c, w, 0, m)), make_double2(a, b));
           }
       }
   }
