@@ -205,7 +205,10 @@ void Operator::build_tasks(const std::vector<RawFace> &faces, const Partition &p
     const int nx = mesh_.cells[0], ny = d_ == 3 ? mesh_.cells[1] : 1;
     const long long layer = (long long)nx * ny;
     const long long b = layout_.owned_begin, e = b + n_owned;
-    const int tile_y = d_ == 3 ? 8 : 1 << 30;
+    int tile_y = d_ == 3 ? 8 : 1 << 30;
+    if (const char *e = std::getenv("DGX_TILE_Y")) // traversal experiments
+      if (d_ == 3 && std::atoi(e) > 0)
+        tile_y = std::atoi(e);
     const int brick0 = (d_ == 3 && precision_ == 0) ? kernel_brick(d_, k_) : 0;
     const int brick = brick0 >= 4 ? brick0 : 0; // 1: x-rows, no reordering
     auto in_range = [&](long long z, int y, int x) {
