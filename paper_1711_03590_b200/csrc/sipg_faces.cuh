@@ -27,6 +27,38 @@ __device__ __forceinline__ void ldg_pair(const Real *un, int p, int m, Real &a, 
     }
 }
 
+// The neighbour pencils through face point p of both faces of axis A
+// (nodal bases), fetched one phase early (across the forward pass's last
+// barrier for axis 0, during the previous axis's test-side passes otherwise)
+template <typename Real, int D, int K, int A>
+__device__ __forceinline__ void nb_fetch_v4(const ApplyParams<Real> &prm, const Real *cell, bool active, int p,
+                                            Real (&x)[2][K])
+{
+  using L = SL<D, K>;
+  constexpr int NQ = L::NQ;
+  int2 tf[2] = {make_int2(-2, 0), make_int2(-2, 0)};
+  if (active)
+    {
+      const int2 *tfs = reinterpret_cast<const int2 *>(cell + L::OFF_TF);
+      tf[0] = tfs[2 * A];
+      tf[1] = tfs[2 * A + 1];
+    }
+#pragma unroll
+  for (int s = 0; s < 2; ++s)
+    {
+      const Real *un = prm.u + (long long)(tf[s].x >= 0 ? tf[s].x : 0) * NQ;
+#pragma unroll
+      for (int m = 0; m + 1 < K; m += 2)
+        {
+          ldg_pair<Real, D, K, A>(un, p, m, x[s][m], x[s][m + 1]);
+          if (tf[s].x < 0)
+            x[s][m] = x[s][m + 1] = Real(0);
+        }
+      if constexpr (K % 2 == 1)
+        x[s][K - 1] = tf[s].x >= 0 ? __ldg(un + gidx<D, K, A>(p, K - 1)) : Real(0);
+    }
+}
+
 // Both faces of axis A of every cell in the CTA (runs before the
 // quadrature-point phase, so G still holds the reference gradient):
 //  own traces      value and reference gradient at the face points from the
@@ -42,9 +74,10 @@ __device__ __forceinline__ void ldg_pair(const Real *un, int p, int m, Real &a, 
 //  test side       w = rv + sum_t Dco_t^T rg_t on the face
 //                  (face_tangential_integrate, :782-788) and rg_A, stored to
 //                  OUT for the backward pass.
-template <typename Real, int D, int K, int A, bool COMPRESSED, bool HERM>
+template <typename Real, int D, int K, int A, bool COMPRESSED, bool HERM, typename HOOK>
 __device__ __forceinline__ void face_axis_v4(const ApplyParams<Real> &prm, Real *cell, int task,
-                                             bool active, int p, Real wf, Real sp)
+                                             bool active, int p, Real wf, Real sp,
+                                             const Real (&xnb)[2][K], HOOK &&before_wpass)
 {
   using L = SL<D, K>;
   using T = TabLayout<K>;
@@ -140,21 +173,7 @@ __device__ __forceinline__ void face_axis_v4(const ApplyParams<Real> &prm, Real 
     }
   else
     {
-      Real x[2][K];
-#pragma unroll
-      for (int s = 0; s < 2; ++s)
-        {
-          const Real *un = prm.u + (long long)(tf[s].x >= 0 ? tf[s].x : 0) * NQ;
-#pragma unroll
-          for (int m = 0; m + 1 < K; m += 2)
-            {
-              ldg_pair<Real, D, K, A>(un, p, m, x[s][m], x[s][m + 1]);
-              if (tf[s].x < 0)
-                x[s][m] = x[s][m + 1] = Real(0);
-            }
-          if constexpr (K % 2 == 1)
-            x[s][K - 1] = tf[s].x >= 0 ? __ldg(un + gidx<D, K, A>(p, K - 1)) : Real(0);
-        }
+      const Real(&x)[2][K] = xnb; // fetched one phase early (nb_fetch_v4)
       NB[fp] = dot_row<Real, K, T::oSf + K>(x[0]);
       NB[FP + fp] = dot_row<Real, K, T::oDf + K>(x[0]);
       NB[2 * FP + fp] = dot_row<Real, K, T::oSf>(x[1]);
@@ -272,6 +291,7 @@ __device__ __forceinline__ void face_axis_v4(const ApplyParams<Real> &prm, Real 
         DT[(2 * t + s) * FP + fp] = g * jo[s][t < A ? t : t + 1];
     }
   __syncthreads();
+  before_wpass();
   // w = rv + sum_t Dco_t^T rg_t, one tangential direction at a time
   for (int t = p; t < 2 * NL; t += P)
     {

@@ -547,6 +547,10 @@ __device__ __forceinline__ void sipg_task(const ApplyParams<Real> &prm, Real *ce
         store_pencil<Real, D, K, 1>(G + FS, p, z);
       }
   }
+  // neighbour pencils of the first face axis, in flight across the barrier
+  Real xnb[2][K];
+  if constexpr (!HERM)
+    nb_fetch_v4<Real, D, K, 0>(prm, cell, active, p, xnb);
   __syncthreads();
 
   // ---- faces ------------------------------------------------------------
@@ -570,10 +574,16 @@ __device__ __forceinline__ void sipg_task(const ApplyParams<Real> &prm, Real *ce
             wf *= wa;
           }
       }
-    face_axis_v4<Real, D, K, 0, COMPRESSED, HERM>(prm, cell, task, active, p, wf, sp);
-    face_axis_v4<Real, D, K, 1, COMPRESSED, HERM>(prm, cell, task, active, p, wf, sp);
+    face_axis_v4<Real, D, K, 0, COMPRESSED, HERM>(prm, cell, task, active, p, wf, sp, xnb, [&] {
+      if constexpr (!HERM)
+        nb_fetch_v4<Real, D, K, 1>(prm, cell, active, p, xnb);
+    });
+    face_axis_v4<Real, D, K, 1, COMPRESSED, HERM>(prm, cell, task, active, p, wf, sp, xnb, [&] {
+      if constexpr (!HERM && D == 3)
+        nb_fetch_v4<Real, D, K, 2>(prm, cell, active, p, xnb);
+    });
     if constexpr (D == 3)
-      face_axis_v4<Real, D, K, 2, COMPRESSED, HERM>(prm, cell, task, active, p, wf, sp);
+      face_axis_v4<Real, D, K, 2, COMPRESSED, HERM>(prm, cell, task, active, p, wf, sp, xnb, [] {});
   }
 #else
   {
@@ -588,6 +598,9 @@ __device__ __forceinline__ void sipg_task(const ApplyParams<Real> &prm, Real *ce
   //      (operators.cpp:669-709); thread p: the points of its pencil along
   //      axis D-1 (coalesced geometry reads, [geo][comp][q] layout)
   {
+    // 3D: t_2 of the thread's own z-pencil stays in registers and the first
+    // backward pass (along z, same pencil) follows without a barrier
+    Real tz[K];
 #pragma unroll
     for (int m = 0; m < K; ++m)
       {
@@ -722,8 +735,17 @@ __device__ __forceinline__ void sipg_task(const ApplyParams<Real> &prm, Real *ce
               t[b] = Real(0);
           }
 #pragma unroll
-        for (int b = 0; b < D; ++b)
+        for (int b = 0; b < (D == 3 ? 2 : D); ++b)
           G[b * FS + q] = t[b];
+        tz[m] = t[D - 1];
+      }
+    if constexpr (D == 3)
+      {
+        // ---- backward, first pass (z): v = Dco_z^T t_2 + z-face terms
+        Real v[K];
+        apply_Dt<Real, K>(tz, v);
+        add_face_terms<Real, D, K, 2>(cell, p, v);
+        store_pencil<Real, D, K, 2>(val, p, v);
       }
   }
   __syncthreads();
@@ -733,11 +755,6 @@ __device__ __forceinline__ void sipg_task(const ApplyParams<Real> &prm, Real *ce
     Real x[K], z[K], v[K];
     if constexpr (D == 3)
       {
-        load_pencil<Real, D, K, 2>(G + 2 * FS, p, x);
-        apply_Dt<Real, K>(x, v);
-        add_face_terms<Real, D, K, 2>(cell, p, v);
-        store_pencil<Real, D, K, 2>(val, p, v);
-        __syncthreads();
         load_pencil<Real, D, K, 1>(G + FS, p, x);
         apply_Dt<Real, K>(x, z);
         load_pencil<Real, D, K, 1>(val, p, v);
