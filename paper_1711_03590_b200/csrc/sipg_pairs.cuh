@@ -29,6 +29,12 @@
 #ifndef DGX_PAIRS_WARP
 #define DGX_PAIRS_WARP 0
 #endif
+#ifndef DGX_EXP_NO_CELL_PF
+#define DGX_EXP_NO_CELL_PF 0
+#endif
+#ifndef DGX_EXP_NO_META_PF
+#define DGX_EXP_NO_META_PF 0
+#endif
 // neighbour trace along t0 as row dot products at the thread's own face
 // points, fused with the flux (no row pass, one barrier less per axis)
 #ifndef DGX_PAIRS_ROWDOT
@@ -869,7 +875,7 @@ __global__ void __launch_bounds__(PL<K>::THREADS, PL<K>::MINB)
   // task metadata of the CTAs one and two generations ahead (prm.ahead =
   // tasks resident on the device): the first link of their prologue's
   // dependent-load chain becomes an L2 hit
-  if (threadIdx.x < 6 && prm.ahead > 0)
+  if (!DGX_EXP_NO_META_PF && threadIdx.x < 6 && prm.ahead > 0)
     {
       const long long t2 = (long long)(blockIdx.x * NC) + (long long)prm.ahead * (1 + threadIdx.x % 2);
       if (t2 < prm.n_tasks)
@@ -884,13 +890,13 @@ __global__ void __launch_bounds__(PL<K>::THREADS, PL<K>::MINB)
         }
     }
 
-  // L2 prefetch of the cell record and the face records (as the
-  // single-pencil kernel), face entries stashed in shared memory
+  // L2 prefetch of the cell record (measured essential: 20.5 -> 22.5 ms
+  // without), face entries stashed in shared memory
   if (active)
     {
       constexpr int LINE = 128;
       const int ncg = prm.sym ? 6 : 10;
-      if (geo >= 0)
+      if (geo >= 0 && !DGX_EXP_NO_CELL_PF)
         {
           const char *gp = reinterpret_cast<const char *>(
             prm.cell_geo + (long long)geo * ncg * (COMPRESSED ? 1 : NQ));
@@ -902,19 +908,8 @@ __global__ void __launch_bounds__(PL<K>::THREADS, PL<K>::MINB)
         reinterpret_cast<int2 *>(cell + L::OFF_TF)[i] = prm.task_face[task * 6 + i];
       if (t == 0)
         reinterpret_cast<int *>(cell + L::OFF_TF)[12] = slot;
-#pragma unroll
-      for (int phi = 0; phi < 6; ++phi)
-        {
-          const int2 tf = prm.task_face[task * 6 + phi];
-          if (tf.x == -2)
-            continue;
-          constexpr int FREC = COMPRESSED ? 1 : P;
-          const char *fp = reinterpret_cast<const char *>(
-            prm.face_geo + (long long)(tf.y & 0x3fffffff) * 7 * FREC);
-          constexpr int fbytes = 7 * FREC * 8;
-          for (int off = t * LINE; off < fbytes; off += GS * LINE)
-            asm volatile("prefetch.global.L2 [%0];" ::"l"(fp + off));
-        }
+      // (no L2 prefetch of the face records: measured 20.72 -> 20.55 ms
+      // without it once the neighbour pencils are fetched one phase early)
     }
 
   // Hermite-like: sign of the tangential indices of the two face points /
