@@ -29,6 +29,9 @@
 #ifndef DGX_PAIRS_WARP
 #define DGX_PAIRS_WARP 0
 #endif
+#ifndef DGX_PAIRS_W1
+#define DGX_PAIRS_W1 1
+#endif
 #ifndef DGX_EXP_NO_CELL_PF
 #define DGX_EXP_NO_CELL_PF 0
 #endif
@@ -70,7 +73,10 @@ struct PL
   static constexpr int FP = K == 6 ? 36 : pr_stride(KP * K, H);
   static constexpr int OFF_G = FS;
   static constexpr int OFF_OUT = 4 * FS;         // 3 axes x (w0, w1, rgn0, rgn1)
-  static constexpr int OFF_NB = OFF_OUT + 12 * FP;
+  // W1: the t1 part Dco_t1^T rg_t1 of the face test values, 3 axes x 2
+  // faces, so that the row and column test passes run in one phase
+  static constexpr int OFF_W1 = OFF_OUT + 12 * FP;
+  static constexpr int OFF_NB = OFF_W1 + (DGX_PAIRS_W1 ? 6 * FP : 0);
   static constexpr int OFF_DT = OFF_NB + 4 * FP;
   static constexpr int OFF_RG1 = OFF_DT + 4 * FP; // row-dot variant: rg along t1, 2 faces
   static constexpr int OFF_TF = OFF_RG1 + (DGX_PAIRS_ROWDOT ? 2 * FP : 0); // 6 int2 face entries
@@ -337,8 +343,17 @@ __device__ __forceinline__ void pr_face_terms(const double *cell, int c, int w, 
   using T = TabLayout<K>;
   const double *OUT = cell + L::OFF_OUT + (2 * A) * 2 * L::FP;
   const int fp = 2 * c + L::FK * w;
-  const double2 w0 = lds2(OUT + fp), w1 = lds2(OUT + L::FP + fp);
+  double2 w0 = lds2(OUT + fp), w1 = lds2(OUT + L::FP + fp);
   const double2 r0 = lds2(OUT + 2 * L::FP + fp), r1 = lds2(OUT + 3 * L::FP + fp);
+  if constexpr (DGX_PAIRS_W1)
+    {
+      const double *W1 = cell + L::OFF_W1 + (2 * A) * L::FP;
+      const double2 u0 = lds2(W1 + fp), u1 = lds2(W1 + L::FP + fp);
+      w0.x += u0.x;
+      w0.y += u0.y;
+      w1.x += u1.x;
+      w1.y += u1.y;
+    }
 #pragma unroll
   for (int m = 0; m < K; ++m)
     {
@@ -780,9 +795,32 @@ __device__ __forceinline__ void pr_face_axis(const ApplyParams<double> &prm, dou
     }
   pr_sync<K>();
   before_wpass();
-  // w = rv + Dco_t0^T rg_t0 (rows) ...
-  for (int tk = t; tk < 2 * K; tk += L::G)
+  // w = rv + Dco_t0^T rg_t0 (rows) ... [W1: and the column tasks below in
+  // the same phase, into W1]
+  for (int tk = t; tk < 2 * K + (DGX_PAIRS_W1 ? 2 * H : 0); tk += L::G)
     {
+      if (DGX_PAIRS_W1 && tk >= 2 * K)
+        {
+          const int tc = tk - 2 * K;
+          const int s = tc / H, a2 = tc - s * H;
+          double *xo = cell + L::OFF_W1 + (2 * A + s) * FP + 2 * a2;
+          const double *yo = DT + (2 + s) * FP + 2 * a2;
+          double y[2][K], b[2][K];
+#pragma unroll
+          for (int m = 0; m < K; ++m)
+            {
+              const double2 u = lds2(yo + FK * m);
+              y[0][m] = u.x;
+              y[1][m] = u.y;
+            }
+#pragma unroll
+          for (int e = 0; e < 2; ++e)
+            apply_Dt<double, K>(y[e], b[e]);
+#pragma unroll
+          for (int m = 0; m < K; ++m)
+            sts2(xo + FK * m, b[0][m], b[1][m]);
+          continue;
+        }
       const int s = tk / K, r = tk - s * K;
       double *xo = OUT + s * FP + FK * r;
       const double *yo = DT + s * FP + FK * r;
@@ -804,6 +842,8 @@ __device__ __forceinline__ void pr_face_axis(const ApplyParams<double> &prm, dou
       for (int j = 0; j < H; ++j)
         sts2(xo + 2 * j, a[2 * j] + b[2 * j], 2 * j + 1 < K ? a[2 * j + 1] + b[2 * j + 1] : 0.0);
     }
+  if constexpr (DGX_PAIRS_W1)
+    return; // no trailing barrier (below)
   pr_sync<K>();
   // ... + Dco_t1^T rg_t1 (column pairs)
   for (int tk = t; tk < 2 * H; tk += L::G)
