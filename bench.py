@@ -69,6 +69,9 @@ VARIANT = {"c4g4": "g4", "c3g4": "g4"}
 BASIS = {"c4h": "hermite_like", "c3h": "hermite_like", "c5h": "hermite_like"}
 # reference instrumented flop count per DoF (counters x W / applies,
 # bench.cpp:339), SURVEY.md s.8d
+# reference counter flops per DoF of C2 (2D, 256^2, Dirichlet) by degree
+C2_FLOPS_PER_DOF = {1: 76.00, 2: 74.67, 3: 86.00, 4: 90.24, 5: 100.00, 6: 105.80, 7: 115.00,
+                    8: 121.48, 9: 130.40, 10: 137.26}
 REF_FLOPS_PER_DOF = {"c4": 240.0, "c3": 215.52, "c5": 260.82, "c5f32": 260.82,
                      "c1": 198.0, "c2": 105.80,
                      # Hermite-like: plain (not even-odd) S passes, same counters
@@ -223,6 +226,8 @@ def main():
     ap.add_argument("--impl", default="dgx", choices=["dgx", "reference"])
     ap.add_argument("--config", default="c4", choices=sorted(CONFIGS))
     ap.add_argument("--cells", type=int, default=None, help="override cells per direction")
+    ap.add_argument("--degree", type=int, default=None,
+                    help="override the polynomial degree (C2 degree sweep p=1..10)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     args = ap.parse_args()
@@ -232,6 +237,9 @@ def main():
     d, n, p, periodic, kind, coef, prec, seed, label = CONFIGS[args.config]
     if args.cells:
         n = args.cells
+    p_config = p
+    if args.degree:
+        p = args.degree
     n_dofs = n ** d * (p + 1) ** d
     metric = ("DG advection apply throughput (DoFs/s)" if ADVECTION.get(args.config)
               else "DG Laplacian apply throughput (DoFs/s)")
@@ -393,7 +401,10 @@ def main():
     # the binding resource: HBM bytes vs FP64 flops (reference counter flops,
     # SURVEY.md s.8d), whichever takes longer at its peak
     fpk, fpk_kind = fp64_peak()
-    flops = REF_FLOPS_PER_DOF.get(args.config, 0.0) * lay.owned_size
+    ref_fpd = REF_FLOPS_PER_DOF.get(args.config, 0.0)
+    if p != p_config:  # degree override: C2's reference counter values per degree
+        ref_fpd = C2_FLOPS_PER_DOF.get(p, 0.0) if args.config == "c2" else 0.0
+    flops = ref_fpd * lay.owned_size
     t_hbm = alg_bytes / (hbm * 1e9)
     t_fp64 = flops / (fpk * 1e12)
     if t_fp64 > t_hbm and prec == "fp64":
@@ -408,7 +419,7 @@ def main():
                     "fp64_tflops": flops / (launch_ms * 1e-3) / 1e12}
     roofline.update({"algorithmic_bytes_per_launch": alg_bytes,
                      "bytes_per_dof": alg_bytes / (lay.owned_size), "launch_ms": launch_ms,
-                     "fp64_flops_per_dof_ref_counters": REF_FLOPS_PER_DOF.get(args.config)})
+                     "fp64_flops_per_dof_ref_counters": ref_fpd or None})
 
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
