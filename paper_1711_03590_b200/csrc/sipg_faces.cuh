@@ -293,6 +293,21 @@ __device__ __forceinline__ void face_axis_v4(const ApplyParams<Real> &prm, Real 
   __syncthreads();
   before_wpass();
   // w = rv + sum_t Dco_t^T rg_t, one tangential direction at a time
+  if constexpr (D == 3 && DGX_V4_W1)
+    {
+      // both directions in one phase: rows accumulate into OUT, columns go
+      // to W1 (summed in add_face_terms)
+      Real *W1 = cell + L::OFF_W1 + (2 * A) * FP;
+      for (int t = p; t < 4 * NL; t += P)
+        {
+          const int s = (t / NL) & 1, l = t % NL;
+          if (t < 2 * NL)
+            line_op<Real, D, K, 0, 3>(OUT + 2 * s * FP, DT + s * FP, l);
+          else
+            line_op<Real, D, K, 1, 4>(W1 + s * FP, DT + (2 + s) * FP, l);
+        }
+      return;
+    }
   for (int t = p; t < 2 * NL; t += P)
     {
       const int s = t / NL, l = t - s * NL;

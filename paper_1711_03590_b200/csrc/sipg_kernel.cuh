@@ -240,6 +240,10 @@ __device__ __forceinline__ unsigned ghost_layer_mask(const int2 *tf, int p)
 // axis 0 -- consecutive threads K entries apart -- are free of fp64 bank
 // conflicts; face fields (k^{d-1} points) likewise use row stride FK.
 // Global (HBM) cell data stays unpadded lexicographic, axis 0 fastest.
+#ifndef DGX_V4_W1
+#define DGX_V4_W1 1
+#endif
+
 template <int D, int K>
 struct SL
 {
@@ -259,6 +263,12 @@ struct SL
   // they stay 8-byte aligned in fp32 too
   static constexpr int OFF_TF = (OFF_DT + 2 * (D - 1) * FP + 1) / 2 * 2;
   static constexpr int SM_CELL = OFF_TF + 4 * D;
+  // apply kernel, 3D: the t1 test parts Dco_t1^T rg_t1 (3 axes x 2 faces)
+  // after the common layout, so that both test-side passes of a face axis
+  // run in one phase (sipg_faces.cuh); the advection / rhs kernels do not
+  // carry it
+  static constexpr int OFF_W1 = (SM_CELL + 1) / 2 * 2;
+  static constexpr int SM_CELL_APPLY = OFF_W1 + (D == 3 && DGX_V4_W1 ? 6 * FP : 0);
 };
 
 // index of the m-th entry along axis A of pencil p (remaining axes
@@ -306,13 +316,13 @@ __device__ __forceinline__ int fln(int l, int m)
     return l + SL<D, K>::FK * m;
 }
 
-template <int D, int K>
+template <int D, int K, bool APPLY = false>
 struct KernelShape
 {
   using L = SL<D, K>;
   static constexpr int P = L::P;
   static constexpr int NQ = L::NQ;
-  static constexpr int SM_CELL = L::SM_CELL;
+  static constexpr int SM_CELL = APPLY ? L::SM_CELL_APPLY : L::SM_CELL;
   // ~160-256 threads per CTA and <= 74 KB of fp64 shared memory, so that
   // three CTAs share one SM (228 KB)
   static constexpr int NC_THREADS = (192 / P) > 0 ? 192 / P : 1;
@@ -378,7 +388,7 @@ __device__ __forceinline__ void line_op(Real *x, Real *y, int l)
       apply_D<Real, K>(b, a);
       store_line<Real, D, K, T>(y, l, a);
     }
-  else
+  else if constexpr (OP == 3)
     {
       Real c[K];
       load_line<Real, D, K, T>(y, l, c);
@@ -388,12 +398,20 @@ __device__ __forceinline__ void line_op(Real *x, Real *y, int l)
         a[m] += b[m];
       store_line<Real, D, K, T>(x, l, a);
     }
+  else
+    {
+      // OP 4: x <- Dco^T y
+      Real c[K];
+      load_line<Real, D, K, T>(y, l, c);
+      apply_Dt<Real, K>(c, b);
+      store_line<Real, D, K, T>(x, l, b);
+    }
 }
 
 // Backward step along axis A: v (pencil) += rf_s w_s + (Dco^T rf_s) rgn_s
 // for both faces of the axis (the transposed own traces, folded as rank-1
 // updates into the pass that already holds the pencil).
-template <typename Real, int D, int K, int A>
+template <typename Real, int D, int K, int A, bool USE_W1 = false>
 __device__ __forceinline__ void add_face_terms(const Real *cell, int p, Real (&v)[K])
 {
   using L = SL<D, K>;
@@ -401,7 +419,13 @@ __device__ __forceinline__ void add_face_terms(const Real *cell, int p, Real (&v
   constexpr int FP = L::FP;
   const Real *OUT = cell + L::OFF_OUT + (2 * A) * 2 * FP;
   const int fp = fpt<D, K>(p);
-  const Real w0 = OUT[fp], r0 = OUT[FP + fp], w1 = OUT[2 * FP + fp], r1 = OUT[3 * FP + fp];
+  Real w0 = OUT[fp], r0 = OUT[FP + fp], w1 = OUT[2 * FP + fp], r1 = OUT[3 * FP + fp];
+  if constexpr (D == 3 && DGX_V4_W1 && USE_W1)
+    {
+      const Real *W1 = cell + L::OFF_W1 + (2 * A) * FP;
+      w0 += W1[fp];
+      w1 += W1[FP + fp];
+    }
 #pragma unroll
   for (int m = 0; m < K; ++m)
     v[m] += tab<Real, K>(T::oRf + m) * w0 + tab<Real, K>(T::oRf + K + m) * w1 +
@@ -744,7 +768,7 @@ __device__ __forceinline__ void sipg_task(const ApplyParams<Real> &prm, Real *ce
         // ---- backward, first pass (z): v = Dco_z^T t_2 + z-face terms
         Real v[K];
         apply_Dt<Real, K>(tz, v);
-        add_face_terms<Real, D, K, 2>(cell, p, v);
+        add_face_terms<Real, D, K, 2, true>(cell, p, v);
         store_pencil<Real, D, K, 2>(val, p, v);
       }
   }
@@ -767,7 +791,7 @@ __device__ __forceinline__ void sipg_task(const ApplyParams<Real> &prm, Real *ce
         load_pencil<Real, D, K, 1>(G + FS, p, x);
         apply_Dt<Real, K>(x, v);
       }
-    add_face_terms<Real, D, K, 1>(cell, p, v);
+    add_face_terms<Real, D, K, 1, true>(cell, p, v);
     store_pencil<Real, D, K, 1>(val, p, v);
     __syncthreads();
     load_pencil<Real, D, K, 0>(G, p, x);
@@ -776,7 +800,7 @@ __device__ __forceinline__ void sipg_task(const ApplyParams<Real> &prm, Real *ce
 #pragma unroll
     for (int m = 0; m < K; ++m)
       v[m] += z[m];
-    add_face_terms<Real, D, K, 0>(cell, p, v);
+    add_face_terms<Real, D, K, 0, true>(cell, p, v);
     apply_St<Real, K>(v, z);
     store_pencil<Real, D, K, 0>(val, p, z);
     __syncthreads();
@@ -804,17 +828,17 @@ __device__ __forceinline__ void sipg_task(const ApplyParams<Real> &prm, Real *ce
 }
 
 template <typename Real, int D, int K, bool COMPRESSED, int BASIS>
-__global__ void __launch_bounds__(KernelShape<D, K>::THREADS, KernelShape<D, K>::MIN_BLOCKS)
+__global__ void __launch_bounds__(KernelShape<D, K, true>::THREADS, KernelShape<D, K, true>::MIN_BLOCKS)
   sipg_apply_kernel(const ApplyParams<Real> prm)
 {
-  using KS = KernelShape<D, K>;
+  using KS = KernelShape<D, K, true>;
   using L = SL<D, K>;
   constexpr int P = L::P, NC = KS::NC;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   Real *smem = reinterpret_cast<Real *>(smem_raw);
   const int lc = threadIdx.x / P;
   const int p = threadIdx.x - lc * P;
-  Real *cell = smem + lc * L::SM_CELL;
+  Real *cell = smem + lc * KS::SM_CELL;
   sipg_task<Real, D, K, COMPRESSED, BASIS>(prm, cell, p, blockIdx.x * NC + lc);
 }
 

@@ -148,7 +148,7 @@ void launch_one(const dev::ApplyParams<Real> &prm, cudaStream_t s)
       launch_pairs<K, C>(prm, s);
       return;
     }
-  using KS = dev::KernelShape<D, K>;
+  using KS = dev::KernelShape<D, K, true>;
   const size_t smem = (size_t)KS::SMEM_REALS * sizeof(Real);
   auto kern = dev::sipg_apply_kernel<Real, D, K, C, DGX_BASIS>;
   static std::set<int> configured;
