@@ -74,7 +74,7 @@ __device__ __forceinline__ void nb_fetch_v4(const ApplyParams<Real> &prm, const 
 //  test side       w = rv + sum_t Dco_t^T rg_t on the face
 //                  (face_tangential_integrate, :782-788) and rg_A, stored to
 //                  OUT for the backward pass.
-template <typename Real, int D, int K, int A, bool COMPRESSED, bool HERM, typename HOOK>
+template <typename Real, int D, int K, int A, bool COMPRESSED, bool HERM, bool GLN, typename HOOK>
 __device__ __forceinline__ void face_axis_v4(const ApplyParams<Real> &prm, Real *cell, int task,
                                              bool active, int p, Real wf, Real sp,
                                              const Real (&xnb)[2][K], HOOK &&before_wpass)
@@ -174,9 +174,10 @@ __device__ __forceinline__ void face_axis_v4(const ApplyParams<Real> &prm, Real 
   else
     {
       const Real(&x)[2][K] = xnb; // fetched one phase early (nb_fetch_v4)
-      NB[fp] = dot_row<Real, K, T::oSf + K>(x[0]);
+      // Gauss-Lobatto nodes: the value rows Sf are exact unit vectors
+      NB[fp] = GLN ? x[0][K - 1] : dot_row<Real, K, T::oSf + K>(x[0]);
       NB[FP + fp] = dot_row<Real, K, T::oDf + K>(x[0]);
-      NB[2 * FP + fp] = dot_row<Real, K, T::oSf>(x[1]);
+      NB[2 * FP + fp] = GLN ? x[1][0] : dot_row<Real, K, T::oSf>(x[1]);
       NB[3 * FP + fp] = dot_row<Real, K, T::oDf>(x[1]);
     }
   // own traces from the collocation fields along the normal

@@ -598,16 +598,16 @@ __device__ __forceinline__ void sipg_task(const ApplyParams<Real> &prm, Real *ce
             wf *= wa;
           }
       }
-    face_axis_v4<Real, D, K, 0, COMPRESSED, HERM>(prm, cell, task, active, p, wf, sp, xnb, [&] {
+    face_axis_v4<Real, D, K, 0, COMPRESSED, HERM, BASIS == 0>(prm, cell, task, active, p, wf, sp, xnb, [&] {
       if constexpr (!HERM)
         nb_fetch_v4<Real, D, K, 1>(prm, cell, active, p, xnb);
     });
-    face_axis_v4<Real, D, K, 1, COMPRESSED, HERM>(prm, cell, task, active, p, wf, sp, xnb, [&] {
+    face_axis_v4<Real, D, K, 1, COMPRESSED, HERM, BASIS == 0>(prm, cell, task, active, p, wf, sp, xnb, [&] {
       if constexpr (!HERM && D == 3)
         nb_fetch_v4<Real, D, K, 2>(prm, cell, active, p, xnb);
     });
     if constexpr (D == 3)
-      face_axis_v4<Real, D, K, 2, COMPRESSED, HERM>(prm, cell, task, active, p, wf, sp, xnb, [] {});
+      face_axis_v4<Real, D, K, 2, COMPRESSED, HERM, BASIS == 0>(prm, cell, task, active, p, wf, sp, xnb, [] {});
   }
 #else
   {

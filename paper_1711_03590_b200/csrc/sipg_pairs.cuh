@@ -428,7 +428,7 @@ __device__ __forceinline__ void pr_nb_fetch(const ApplyParams<double> &prm, cons
 // Both faces of axis A (same algebra as face_axis_v4, sipg_faces.cuh, with
 // the pair mapping): own traces, neighbour trace, SIPG flux
 // (operators.cpp:977-1003 interior, 1069-1089 boundary), test side.
-template <int K, int A, bool COMPRESSED, bool HERM, typename HOOK>
+template <int K, int A, bool COMPRESSED, bool HERM, bool GLN, typename HOOK>
 __device__ __forceinline__ void pr_face_axis(const ApplyParams<double> &prm, double *cell, bool active,
                                              int c, int w, int t, int lc, const double (&wf)[2],
                                              const double (&sp)[2], const double (&xnb)[2][2][K],
@@ -493,9 +493,17 @@ __device__ __forceinline__ void pr_face_axis(const ApplyParams<double> &prm, dou
   else
     {
       const double(&x)[2][2][K] = xnb; // fetched one phase early (pr_nb_fetch)
-      sts2(NB + fp, dot_row<double, K, T::oSf + K>(x[0][0]), dot_row<double, K, T::oSf + K>(x[0][1]));
+      // Gauss-Lobatto nodes: the value rows Sf are exact unit vectors (the
+      // end nodes), so the neighbour's face value is its end-node value
+      if constexpr (GLN)
+        sts2(NB + fp, x[0][0][K - 1], x[0][1][K - 1]);
+      else
+        sts2(NB + fp, dot_row<double, K, T::oSf + K>(x[0][0]), dot_row<double, K, T::oSf + K>(x[0][1]));
       sts2(NB + FP + fp, dot_row<double, K, T::oDf + K>(x[0][0]), dot_row<double, K, T::oDf + K>(x[0][1]));
-      sts2(NB + 2 * FP + fp, dot_row<double, K, T::oSf>(x[1][0]), dot_row<double, K, T::oSf>(x[1][1]));
+      if constexpr (GLN)
+        sts2(NB + 2 * FP + fp, x[1][0][0], x[1][1][0]);
+      else
+        sts2(NB + 2 * FP + fp, dot_row<double, K, T::oSf>(x[1][0]), dot_row<double, K, T::oSf>(x[1][1]));
       sts2(NB + 3 * FP + fp, dot_row<double, K, T::oDf>(x[1][0]), dot_row<double, K, T::oDf>(x[1][1]));
     }
   // own traces from the collocation fields along the normal
@@ -1082,15 +1090,15 @@ __global__ void __launch_bounds__(PL<K>::THREADS, PL<K>::MINB)
     if (false)
 #endif
     {
-    pr_face_axis<K, 0, COMPRESSED, HERM>(prm, cell, active, c, w, t, lc, wf, sp, xnb, [&] {
+    pr_face_axis<K, 0, COMPRESSED, HERM, BASIS == 0>(prm, cell, active, c, w, t, lc, wf, sp, xnb, [&] {
       if constexpr (!HERM)
         pr_nb_fetch<K, 1>(prm, cell, active, c, w, lc, xnb);
     });
-    pr_face_axis<K, 1, COMPRESSED, HERM>(prm, cell, active, c, w, t, lc, wf, sp, xnb, [&] {
+    pr_face_axis<K, 1, COMPRESSED, HERM, BASIS == 0>(prm, cell, active, c, w, t, lc, wf, sp, xnb, [&] {
       if constexpr (!HERM)
         pr_nb_fetch<K, 2>(prm, cell, active, c, w, lc, xnb);
     });
-    pr_face_axis<K, 2, COMPRESSED, HERM>(prm, cell, active, c, w, t, lc, wf, sp, xnb, [&] {
+    pr_face_axis<K, 2, COMPRESSED, HERM, BASIS == 0>(prm, cell, active, c, w, t, lc, wf, sp, xnb, [&] {
 #pragma unroll
       for (int m = 0; m < QD - 1; ++m)
         load_layer(m);
