@@ -136,6 +136,22 @@ __device__ __forceinline__ void face_axis_v4(const ApplyParams<Real> &prm, Real 
           tau[s] = __ldg(prm.penalty + fid);
         }
     }
+  // own traces from the collocation fields along the normal (first: their
+  // shared-memory loads overlap the arrival of the neighbour pencils)
+  Real own_u[2], own_g[2][D];
+  {
+    Real x[K];
+    load_pencil<Real, D, K, A>(val, p, x);
+    own_u[0] = dot_row<Real, K, T::oRf>(x);
+    own_u[1] = dot_row<Real, K, T::oRf + K>(x);
+#pragma unroll
+    for (int b = 0; b < D; ++b)
+      {
+        load_pencil<Real, D, K, A>(G + b * FS, p, x);
+        own_g[0][b] = dot_row<Real, K, T::oRf>(x);
+        own_g[1][b] = dot_row<Real, K, T::oRf + K>(x);
+      }
+  }
   // neighbour pencils -> nodal value / normal-derivative layer (own low face
   // meets the neighbour's high face, row index 1, and vice versa). Both
   // neighbours' loads are issued before either is used: one memory latency
@@ -180,21 +196,6 @@ __device__ __forceinline__ void face_axis_v4(const ApplyParams<Real> &prm, Real 
       NB[2 * FP + fp] = GLN ? x[1][0] : dot_row<Real, K, T::oSf>(x[1]);
       NB[3 * FP + fp] = dot_row<Real, K, T::oDf>(x[1]);
     }
-  // own traces from the collocation fields along the normal
-  Real own_u[2], own_g[2][D];
-  {
-    Real x[K];
-    load_pencil<Real, D, K, A>(val, p, x);
-    own_u[0] = dot_row<Real, K, T::oRf>(x);
-    own_u[1] = dot_row<Real, K, T::oRf + K>(x);
-#pragma unroll
-    for (int b = 0; b < D; ++b)
-      {
-        load_pencil<Real, D, K, A>(G + b * FS, p, x);
-        own_g[0][b] = dot_row<Real, K, T::oRf>(x);
-        own_g[1][b] = dot_row<Real, K, T::oRf + K>(x);
-      }
-  }
   __syncthreads();
 
   if constexpr (D == 3)

@@ -453,6 +453,30 @@ __device__ __forceinline__ void pr_face_axis(const ApplyParams<double> &prm, dou
   bool inr[2];
   const double *PNB[2];
   pr_axis_faces<K, A>(cell, active, lc, tf, inr, PNB);
+  // own traces from the collocation fields along the normal (first: their
+  // shared-memory loads overlap the arrival of the neighbour pencils)
+  double own_u[2][2], own_g[2][2][3];
+  {
+    double x[2][K];
+    pr_load<K, A>(val, c, w, x);
+#pragma unroll
+    for (int e = 0; e < 2; ++e)
+      {
+        own_u[0][e] = dot_row<double, K, T::oRf>(x[e]);
+        own_u[1][e] = dot_row<double, K, T::oRf + K>(x[e]);
+      }
+#pragma unroll
+    for (int b = 0; b < 3; ++b)
+      {
+        pr_load<K, A>(G + b * FS, c, w, x);
+#pragma unroll
+        for (int e = 0; e < 2; ++e)
+          {
+            own_g[0][e][b] = dot_row<double, K, T::oRf>(x[e]);
+            own_g[1][e][b] = dot_row<double, K, T::oRf + K>(x[e]);
+          }
+      }
+  }
   // neighbour nodal value / normal-derivative layers at the two points
   if constexpr (HERM)
     {
@@ -506,29 +530,6 @@ __device__ __forceinline__ void pr_face_axis(const ApplyParams<double> &prm, dou
         sts2(NB + 2 * FP + fp, dot_row<double, K, T::oSf>(x[1][0]), dot_row<double, K, T::oSf>(x[1][1]));
       sts2(NB + 3 * FP + fp, dot_row<double, K, T::oDf>(x[1][0]), dot_row<double, K, T::oDf>(x[1][1]));
     }
-  // own traces from the collocation fields along the normal
-  double own_u[2][2], own_g[2][2][3];
-  {
-    double x[2][K];
-    pr_load<K, A>(val, c, w, x);
-#pragma unroll
-    for (int e = 0; e < 2; ++e)
-      {
-        own_u[0][e] = dot_row<double, K, T::oRf>(x[e]);
-        own_u[1][e] = dot_row<double, K, T::oRf + K>(x[e]);
-      }
-#pragma unroll
-    for (int b = 0; b < 3; ++b)
-      {
-        pr_load<K, A>(G + b * FS, c, w, x);
-#pragma unroll
-        for (int e = 0; e < 2; ++e)
-          {
-            own_g[0][e][b] = dot_row<double, K, T::oRf>(x[e]);
-            own_g[1][e][b] = dot_row<double, K, T::oRf + K>(x[e]);
-          }
-      }
-  }
   // own side n.J^{-T} at the two points; the own gradient trace is only
   // needed projected on it (dn_own), which frees its registers early
   double jo[2][2][3], dn_own[2][2];
