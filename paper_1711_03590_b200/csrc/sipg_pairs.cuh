@@ -453,6 +453,43 @@ __device__ __forceinline__ void pr_face_axis(const ApplyParams<double> &prm, dou
   bool inr[2];
   const double *PNB[2];
   pr_axis_faces<K, A>(cell, active, lc, tf, inr, PNB);
+  // own side n.J^{-T} at the two points (issued first: used right after the
+  // own traces, as dn_own = n.J^{-T} grad u)
+  double jo[2][2][3], dn_own[2][2];
+#pragma unroll
+  for (int s = 0; s < 2; ++s)
+    {
+#pragma unroll
+      for (int e = 0; e < 2; ++e)
+#pragma unroll
+        for (int b = 0; b < 3; ++b)
+          jo[s][e][b] = 0.0;
+      if (tf[s].x != -2)
+        {
+          const int fid = tf[s].y & 0x3fffffff;
+          const int side = (tf[s].y >> 30) & 1;
+          if constexpr (COMPRESSED)
+            {
+              const double *fg = prm.face_geo + (long long)fid * 7;
+#pragma unroll
+              for (int e = 0; e < 2; ++e)
+#pragma unroll
+                for (int b = 0; b < 3; ++b)
+                  jo[s][e][b] = __ldg(fg + 1 + side * 3 + b);
+            }
+          else
+            {
+              const double *fg = prm.face_geo + (long long)fid * 7 * P + fpg;
+#pragma unroll
+              for (int b = 0; b < 3; ++b)
+                {
+                  const double2 o = pr_ldg_pt<K>(fg + (1 + side * 3 + b) * P, p1);
+                  jo[s][0][b] = o.x;
+                  jo[s][1][b] = o.y;
+                }
+            }
+        }
+    }
   // own traces from the collocation fields along the normal (first: their
   // shared-memory loads overlap the arrival of the neighbour pencils)
   double own_u[2][2], own_g[2][2][3];
@@ -530,42 +567,11 @@ __device__ __forceinline__ void pr_face_axis(const ApplyParams<double> &prm, dou
         sts2(NB + 2 * FP + fp, dot_row<double, K, T::oSf>(x[1][0]), dot_row<double, K, T::oSf>(x[1][1]));
       sts2(NB + 3 * FP + fp, dot_row<double, K, T::oDf>(x[1][0]), dot_row<double, K, T::oDf>(x[1][1]));
     }
-  // own side n.J^{-T} at the two points; the own gradient trace is only
-  // needed projected on it (dn_own), which frees its registers early
-  double jo[2][2][3], dn_own[2][2];
+  // the own gradient trace is only needed projected on n.J^{-T} (dn_own),
+  // which frees its registers early
 #pragma unroll
   for (int s = 0; s < 2; ++s)
     {
-#pragma unroll
-      for (int e = 0; e < 2; ++e)
-#pragma unroll
-        for (int b = 0; b < 3; ++b)
-          jo[s][e][b] = 0.0;
-      if (tf[s].x != -2)
-        {
-          const int fid = tf[s].y & 0x3fffffff;
-          const int side = (tf[s].y >> 30) & 1;
-          if constexpr (COMPRESSED)
-            {
-              const double *fg = prm.face_geo + (long long)fid * 7;
-#pragma unroll
-              for (int e = 0; e < 2; ++e)
-#pragma unroll
-                for (int b = 0; b < 3; ++b)
-                  jo[s][e][b] = __ldg(fg + 1 + side * 3 + b);
-            }
-          else
-            {
-              const double *fg = prm.face_geo + (long long)fid * 7 * P + fpg;
-#pragma unroll
-              for (int b = 0; b < 3; ++b)
-                {
-                  const double2 o = pr_ldg_pt<K>(fg + (1 + side * 3 + b) * P, p1);
-                  jo[s][0][b] = o.x;
-                  jo[s][1][b] = o.y;
-                }
-            }
-        }
 #pragma unroll
       for (int e = 0; e < 2; ++e)
         dn_own[s][e] = own_g[s][e][0] * jo[s][e][0] + own_g[s][e][1] * jo[s][e][1] +
