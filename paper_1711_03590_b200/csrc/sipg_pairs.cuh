@@ -988,6 +988,10 @@ __global__ void __launch_bounds__(PL<K>::THREADS, PL<K>::MINB)
         }
     }
 
+  // neighbour pencils of the first face axis: issued with the cell's own u
+  // (the stashed face entries are visible after the forward's first barrier,
+  // so the fetch happens right after it), in flight across the forward pass
+  double xnb[2][2][K];
   // ---- forward: val = (S x S x S) u, G_b = Dco_b val ----------------------
   {
     double x[2][K], z[2][K];
@@ -1011,6 +1015,8 @@ __global__ void __launch_bounds__(PL<K>::THREADS, PL<K>::MINB)
       apply_S<double, K>(x[e], z[e]);
     pr_store<K, 2>(val, c, w, z);
     pr_sync<K>();
+    if constexpr (!HERM)
+      pr_nb_fetch<K, 0>(prm, cell, active, c, w, lc, xnb);
     pr_load<K, 0>(val, cx, wx, x);
 #pragma unroll
     for (int e = 0; e < 2; ++e)
@@ -1038,10 +1044,6 @@ __global__ void __launch_bounds__(PL<K>::THREADS, PL<K>::MINB)
       apply_D<double, K>(x[e], z[e]);
     pr_store<K, 2>(G + 2 * FS, c, w, z);
   }
-  // neighbour pencils of the first face axis, in flight across the barrier
-  double xnb[2][2][K];
-  if constexpr (!HERM)
-    pr_nb_fetch<K, 0>(prm, cell, active, c, w, lc, xnb);
   pr_sync<K>();
 
   // cell record of the quadrature-point operation: its first point layers
