@@ -45,8 +45,10 @@ if os.environ.get("PAIRS"):
     KB_PAIRS = dict(prologue=(_ln("sipg_pairs_kernel(const"), _ln("// ---- forward")), forward=(_ln("// ---- forward"), _ln("// ---- faces")),
                     faces=(_ln("// ---- faces"), _ln("// ---- quadrature-point")), qop=(_ln("// ---- quadrature-point"), _ln("// ---- backward")),
                     backward=(_ln("// ---- backward"), len(src)))
-    FB_PAIRS = dict(nbload=(_ln("// neighbour nodal value"), _ln("// own traces")), own=(_ln("// own traces"), _ln("// own side n.J")),
-                    pass12=(_ln("// pass 1,"), _ln("// flux at the two")), fgeo=(_ln("// rest of the face geometry"), _ln("// pass 2,")), jo=(_ln("// own side n.J"), _ln("// pass 1,")),
+    FB_PAIRS = dict(jo=(_ln("// own side n.J"), _ln("// own traces")), own=(_ln("// own traces"), _ln("// neighbour nodal value")),
+                    nbload=(_ln("// neighbour nodal value"), _ln("// the own gradient trace is only")),
+                    dn=(_ln("// the own gradient trace is only"), _ln("// pass 1,")),
+                    pass12=(_ln("// pass 1,"), _ln("// flux at the two")), fgeo=(_ln("// rest of the face geometry"), _ln("// pass 2,")),
                     flux=(_ln("// flux at the two"), _ln("// w = rv")), wpass=(_ln("// w = rv"), _ln("// no trailing barrier")))
     KB, FB = KB_PAIRS, FB_PAIRS
 
