@@ -218,6 +218,23 @@ RANDOM = [
     (3, [2, 3, 3], 3, True, None, False, 1),
     (3, [6, 2, 2], 7, False, ("vertex", 0.1), True, 2),
     (3, [7, 2, 1], 9, True, ("reference", 0.04, 2), False, 1),
+    # degenerate meshes: one periodic cell (each face pairs the cell with
+    # itself; in the pair kernel the x partner is the cell itself), two cells
+    # periodic in x (partner and periodic neighbour coincide), one-cell-thick
+    # slabs, a single Dirichlet cell
+    (3, [1, 1, 1], 5, True, None, False, 1),
+    (3, [1, 1, 1], 4, True, None, False, 1),
+    (3, [2, 1, 1], 3, True, None, False, 1),
+    (3, [2, 1, 1], 5, True, ("vertex", 0.1), True, 1),
+    (3, [1, 2, 1], 1, True, None, False, 1),
+    (3, [1, 1, 1], 2, False, None, False, 1),
+    (2, [1, 1], 4, True, None, False, 1),
+    (2, [1, 9], 5, True, None, False, 1),
+    (2, [9, 1], 3, True, ("vertex", 0.1), False, 1),
+    # one cell per rank, periodic: a rank's two z neighbours are one ghost cell
+    (3, [1, 1, 2], 3, True, None, False, 2),
+    (3, [1, 1, 3], 5, True, None, False, 3),
+    (2, [2, 1], 5, True, None, False, 2),
 ]
 
 
@@ -249,6 +266,10 @@ RANDOM_BASES = [
     (3, [3, 3, 2], 2, False, ("reference", 0.04, 2), False, 2, "lagrange_gauss"),
     (3, [3, 2, 2], 5, True, None, False, 1, "lagrange_gauss"),
     (2, [5, 4], 7, False, ("vertex", 0.1), True, 3, "lagrange_gauss"),
+    # degenerate meshes (one periodic cell; one cell per rank)
+    (3, [1, 1, 1], 4, True, None, False, 1, "hermite_like"),
+    (3, [1, 1, 2], 4, True, None, False, 2, "hermite_like"),
+    (3, [1, 1, 1], 3, True, None, False, 1, "lagrange_gauss"),
 ]
 
 
