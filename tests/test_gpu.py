@@ -661,6 +661,11 @@ ADV_RANDOM = [
     (3, [3, 3, 3], 4, False, 0.0, 1, 2, (0.85, 0.6, 0.35), 0, "gl"),
     (3, [3, 3, 2], 3, False, 0.05, 2, 2, (0.0, 0.0, 0.0), 1, "gl"),
     (2, [4, 4], 6, False, 0.05, 2, 1, (0.0, 0.0, 0.0), 1, "gauss"),
+    # degenerate meshes: one periodic cell (upwind flux of the cell with
+    # itself), one cell per rank (both z neighbours are one ghost cell)
+    (3, [1, 1, 1], 3, True, 0.0, 1, 1, (0.85, 0.6, 0.35), 0, "gl"),
+    (3, [1, 1, 2], 4, True, 0.0, 1, 2, (-0.3, 0.8, 0.5), 0, "gl"),
+    (2, [1, 1], 5, False, 0.0, 1, 1, (0.5, -0.5, 0.0), 0, "gl"),
 ]
 
 
