@@ -413,6 +413,42 @@ def test_fp32_against_fp64_reference(torch, name):
     assert rel_l2(y, c.g[f"y{s}"]) < TOL32
 
 
+FP32_RANDOM = [
+    # d, cells, p, periodic, deform, coefficient, basis (single rank)
+    (3, [3, 3, 2], 5, False, ("vertex", 0.1), True, "lagrange_gauss_lobatto"),
+    (3, [2, 2, 2], 4, True, ("reference", 0.04, 2), False, "lagrange_gauss_lobatto"),
+    (2, [5, 4], 7, False, ("vertex", 0.1), False, "lagrange_gauss_lobatto"),
+    (3, [3, 2, 2], 6, True, None, False, "hermite_like"),
+    # degenerate meshes
+    (3, [1, 1, 1], 5, True, None, False, "lagrange_gauss_lobatto"),
+    (3, [2, 1, 1], 4, True, None, False, "lagrange_gauss_lobatto"),
+    (2, [1, 1], 3, True, None, False, "lagrange_gauss_lobatto"),
+]
+
+
+@pytest.mark.parametrize("cfg", FP32_RANDOM, ids=lambda c: f"d{c[0]}p{c[2]}{c[6][:4]}")
+def test_fp32_random_against_oracle(torch, cfg):
+    """The fp32 apply (dgx_apply_f32) against the fp64 oracle, TOL32 in rel L2."""
+    from oracle import oracle as O
+    D = dgx()
+    d, cells, p, periodic, deform, coef, basis = cfg
+    P = O.Problem(d, cells, p, periodic=periodic, deform=deform, coefficient=coef, n_ranks=1,
+                  basis=O.BASIS[basis])
+    amp = deform[1] if deform and deform[0] == "reference" else 0.0
+    m = deform[2] if deform and deform[0] == "reference" else 1
+    mesh = D.make_box_mesh(d, cells, amp, periodic, m)
+    faces = D.enumerate_faces(mesh)
+    part = D.partition_cells(mesh, 1)
+    D.assign_face_owners(mesh, faces, part)
+    geo = (D.Geometry(source="vertex_bump", vertex_bump_eps=deform[1], coefficient="a1" if coef else None)
+           if deform and deform[0] == "vertex" else D.Geometry(source="mesh"))
+    op = D.RankOperator(mesh, part, faces, geo,
+                        D.OperatorConfig(d=d, p=p, precision="fp32", basis=basis), 0)
+    x = O.random_vector(P.n_dofs, 3000 + p)
+    y = apply_single(torch, op, x, dtype=torch.float32)
+    assert rel_l2(y, P.apply(x)) < TOL32
+
+
 def big_problem(torch, d, n, p, periodic, geometry):
     D = dgx()
     mesh = D.make_box_mesh(d, n, 0.0, periodic, 1)
