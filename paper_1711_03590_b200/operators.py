@@ -295,11 +295,25 @@ class RankOperator:
     def apply(self, u, y, hooks=None, stream=None):
         """y = A u (operators.cpp:217-264). u, y: CUDA tensors (float64, or
         float32 for precision='fp32') of layout().total_size values."""
+        self._check_vectors(u, y)
         hk = None if hooks is None else C.byref(hooks.c_hooks())
         fn = lib().dgx_apply_f32 if self.config.precision == "fp32" else lib().dgx_apply
         check(fn(self._h, _ptr(u), _ptr(y), hk, _stream(stream)))
 
+    def _check_vectors(self, *vs):
+        """Tensor arguments: layout().total_size values of the operator's
+        precision ("apply: vector size mismatch", operators.cpp:220-222).
+        Raw integer pointers are passed through unchecked, as in the C ABI."""
+        want = "torch.float32" if self.config.precision == "fp32" else "torch.float64"
+        for v in vs:
+            if hasattr(v, "data_ptr"):
+                if v.numel() != self._layout.total_size:
+                    raise _lib.DgxInvalidArgument("apply: vector size mismatch")
+                if str(v.dtype) != want:
+                    raise _lib.DgxInvalidArgument(f"apply: {want[6:]} vectors expected")
+
     def apply_phase(self, phase, u, y, stream=None):
+        self._check_vectors(u, y)
         check(lib().dgx_apply_phase(self._h, C.c_int(phase), _ptr(u), _ptr(y),
                                     _stream(stream)))
 

@@ -837,3 +837,29 @@ def test_geometry_variant_g4_host_arrays(torch):
                         D.OperatorConfig(d=d, p=p, geometry="g4"), 0)
     y = apply_single(torch, op, x)
     assert rel_linf(y, w.apply(x)) < TOL64
+
+
+def test_apply_argument_errors(torch):
+    """apply's argument checks (operators.cpp:220-222: "apply: vector size
+    mismatch" is std::invalid_argument) raise before any launch; the operator
+    still applies correctly afterwards."""
+    D = dgx()
+    from paper_1711_03590_b200 import _lib
+    op = big_problem(torch, 3, 2, 3, True, D.Geometry())
+    N = op.layout().total_size
+    u = torch.rand(N, dtype=torch.float64, device="cuda")
+    y = torch.empty_like(u)
+    with pytest.raises(_lib.DgxInvalidArgument, match="size mismatch"):
+        op.apply(u[:-1], y)
+    with pytest.raises(_lib.DgxInvalidArgument, match="size mismatch"):
+        op.apply(u, torch.empty(N + 1, dtype=torch.float64, device="cuda"))
+    with pytest.raises(_lib.DgxInvalidArgument, match="float64"):
+        op.apply(u.float(), y)
+    with pytest.raises(_lib.DgxInvalidArgument, match="GPU"):
+        op.apply(u.cpu(), y)
+    with pytest.raises(_lib.DgxInvalidArgument, match="contiguous"):
+        op.apply(torch.rand(2 * N, dtype=torch.float64, device="cuda")[::2], y)
+    op.apply(u, y)
+    y2 = torch.empty_like(u)
+    op.apply(u, y2)
+    assert torch.equal(y, y2)
