@@ -863,3 +863,40 @@ def test_apply_argument_errors(torch):
     y2 = torch.empty_like(u)
     op.apply(u, y2)
     assert torch.equal(y, y2)
+
+
+GUARD_CASES = [c for c in RANDOM if c[6] == 1 and (min(c[1]) == 1 or c[2] in (4, 5))]
+
+
+@pytest.mark.parametrize("cfg", GUARD_CASES, ids=_cfg_id)
+def test_guard_bands(torch, cfg):
+    """Out-of-bounds check without a sanitizer: u sits between NaN guard bands
+    (any read past either end reaches y as NaN) and y between sentinel bands
+    (any write past either end changes them); y must match the oracle."""
+    from oracle import oracle as O
+    D = dgx()
+    d, cells, p, periodic, deform, coef, _ = cfg[:7]
+    P = O.Problem(d, cells, p, periodic=periodic, deform=deform, coefficient=coef, n_ranks=1,
+                  basis=O.BASIS["lagrange_gauss_lobatto"])
+    amp = deform[1] if deform and deform[0] == "reference" else 0.0
+    m = deform[2] if deform and deform[0] == "reference" else 1
+    mesh = D.make_box_mesh(d, cells, amp, periodic, m)
+    faces = D.enumerate_faces(mesh)
+    part = D.partition_cells(mesh, 1)
+    D.assign_face_owners(mesh, faces, part)
+    geo = (D.Geometry(source="vertex_bump", vertex_bump_eps=deform[1], coefficient="a1" if coef else None)
+           if deform and deform[0] == "vertex" else D.Geometry(source="mesh"))
+    op = D.RankOperator(mesh, part, faces, geo, D.OperatorConfig(d=d, p=p), 0)
+    N = op.layout().total_size
+    pad = 4096
+    x = O.random_vector(P.n_dofs, 5000 + p)
+    ub = torch.full((N + 2 * pad,), float("nan"), dtype=torch.float64, device="cuda")
+    yb = torch.full((N + 2 * pad,), 12345.0, dtype=torch.float64, device="cuda")
+    ub[pad:pad + N] = torch.from_numpy(x).cuda()
+    op.apply(ub[pad:pad + N], yb[pad:pad + N])
+    torch.cuda.synchronize()
+    assert bool((yb[:pad] == 12345.0).all()) and bool((yb[pad + N:] == 12345.0).all())
+    y = yb[pad:pad + N].cpu().numpy()
+    assert np.isfinite(y).all()
+    y_ref = P.apply(x)
+    assert rel_linf(y, y_ref) < TOL64
