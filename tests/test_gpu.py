@@ -865,7 +865,8 @@ def test_apply_argument_errors(torch):
     assert torch.equal(y, y2)
 
 
-GUARD_CASES = [c for c in RANDOM if c[6] == 1 and (min(c[1]) == 1 or c[2] in (4, 5))]
+GUARD_CASES = ([c for c in RANDOM if c[6] == 1 and (min(c[1]) == 1 or c[2] in (4, 5))]
+               + [c for c in RANDOM_BASES if c[6] == 1 and (min(c[1]) == 1 or c[2] in (4, 5, 8))])
 
 
 @pytest.mark.parametrize("cfg", GUARD_CASES, ids=_cfg_id)
@@ -876,8 +877,9 @@ def test_guard_bands(torch, cfg):
     from oracle import oracle as O
     D = dgx()
     d, cells, p, periodic, deform, coef, _ = cfg[:7]
+    basis = cfg[7] if len(cfg) > 7 else "lagrange_gauss_lobatto"
     P = O.Problem(d, cells, p, periodic=periodic, deform=deform, coefficient=coef, n_ranks=1,
-                  basis=O.BASIS["lagrange_gauss_lobatto"])
+                  basis=O.BASIS[basis])
     amp = deform[1] if deform and deform[0] == "reference" else 0.0
     m = deform[2] if deform and deform[0] == "reference" else 1
     mesh = D.make_box_mesh(d, cells, amp, periodic, m)
@@ -886,7 +888,7 @@ def test_guard_bands(torch, cfg):
     D.assign_face_owners(mesh, faces, part)
     geo = (D.Geometry(source="vertex_bump", vertex_bump_eps=deform[1], coefficient="a1" if coef else None)
            if deform and deform[0] == "vertex" else D.Geometry(source="mesh"))
-    op = D.RankOperator(mesh, part, faces, geo, D.OperatorConfig(d=d, p=p), 0)
+    op = D.RankOperator(mesh, part, faces, geo, D.OperatorConfig(d=d, p=p, basis=basis), 0)
     N = op.layout().total_size
     pad = 4096
     x = O.random_vector(P.n_dofs, 5000 + p)
