@@ -902,3 +902,29 @@ def test_guard_bands(torch, cfg):
     assert np.isfinite(y).all()
     y_ref = P.apply(x)
     assert rel_linf(y, y_ref) < TOL64
+
+
+@pytest.mark.parametrize("shape", [("C3", 64, 4, "vertex"), ("C4", 128, 5, "vertex_a"),
+                                   ("C5", 160, 6, "cart")], ids=lambda s: s[0])
+def test_guard_bands_full_size(torch, shape):
+    """The guard-band check at the bench sizes (production grids of the
+    pencil-pair and single-pencil kernels): no read past u, no write past y;
+    y equals the unguarded apply bitwise."""
+    name, n, p, kind = shape
+    D = dgx()
+    geo = (D.Geometry(source="vertex_bump", vertex_bump_eps=0.1,
+                      coefficient="a1" if kind == "vertex_a" else None)
+           if kind.startswith("vertex") else D.Geometry())
+    op = big_problem(torch, 3, n, p, False, geo)
+    N = op.layout().total_size
+    pad = 1 << 16
+    g = torch.Generator(device="cuda").manual_seed(9)
+    ub = torch.full((N + 2 * pad,), float("nan"), dtype=torch.float64, device="cuda")
+    ub[pad:pad + N] = torch.rand(N, dtype=torch.float64, device="cuda", generator=g)
+    yb = torch.full((N + 2 * pad,), 12345.0, dtype=torch.float64, device="cuda")
+    op.apply(ub[pad:pad + N], yb[pad:pad + N])
+    y0 = torch.empty(N, dtype=torch.float64, device="cuda")
+    op.apply(ub[pad:pad + N].clone(), y0)
+    assert bool((yb[:pad] == 12345.0).all()) and bool((yb[pad + N:] == 12345.0).all())
+    assert torch.equal(yb[pad:pad + N], y0)
+    assert bool(torch.isfinite(y0).all())
