@@ -928,3 +928,38 @@ def test_guard_bands_full_size(torch, shape):
     assert bool((yb[:pad] == 12345.0).all()) and bool((yb[pad + N:] == 12345.0).all())
     assert torch.equal(yb[pad:pad + N], y0)
     assert bool(torch.isfinite(y0).all())
+
+
+@pytest.mark.parametrize("cfg", [c for c in ADV_RANDOM if c[6] == 1],
+                         ids=lambda c: f"d{c[0]}p{c[2]}f{c[8]}-{c[9]}")
+def test_guard_bands_advection(torch, cfg):
+    """Guard bands (NaN around u, sentinels around y) for the advection
+    kernel; y against the reference RankOperator."""
+    from oracle import reflib as R
+    if not R.available():
+        pytest.skip("reference library not built")
+    D = dgx()
+    d, cells, p, periodic, amp, m, nr, vel, field, basis = cfg
+    w = R.World(d, cells, p, n_ranks=1, amplitude=amp, mapping_degree=m, periodic=periodic,
+                basis=basis, kind="advection", velocity=vel, velocity_field=field)
+    x = R.random_vector(w.n_dofs, 6000 + p)
+    mesh = D.make_box_mesh(d, cells, amp, periodic, m)
+    faces = D.enumerate_faces(mesh)
+    part = D.partition_cells(mesh, 1)
+    D.assign_face_owners(mesh, faces, part)
+    cfg_ = D.OperatorConfig(d=d, p=p, kind="advection", velocity=vel,
+                            variable_velocity=bool(field),
+                            basis={"gl": "lagrange_gauss_lobatto", "gauss": "lagrange_gauss"}[basis])
+    op = D.RankOperator(mesh, part, faces, D.Geometry(source="mesh"), cfg_, 0)
+    if field:
+        set_field_velocity(op, d)
+    N = op.layout().total_size
+    pad = 4096
+    ub = torch.full((N + 2 * pad,), float("nan"), dtype=torch.float64, device="cuda")
+    yb = torch.full((N + 2 * pad,), 12345.0, dtype=torch.float64, device="cuda")
+    ub[pad:pad + N] = torch.from_numpy(x).cuda()
+    op.apply(ub[pad:pad + N], yb[pad:pad + N])
+    torch.cuda.synchronize()
+    assert bool((yb[:pad] == 12345.0).all()) and bool((yb[pad + N:] == 12345.0).all())
+    y = yb[pad:pad + N].cpu().numpy()
+    assert rel_linf(y, w.apply(x)) < TOL64
