@@ -263,12 +263,27 @@ typedef struct dgx_solve_report
 dgx_status dgx_conjugate_gradient(dgx_op *op, const double *b, double *x, double rel_tol,
                                   int max_iterations, dgx_solve_report *report, void *stream);
 
-/* ---- native NCCL transport (replaces GhostExchanger, ghost_exchange.hpp:
- * 96-128, over NVLink instead of in-process queues) ---------------------- */
+/* ---- native exchanger (replaces GhostExchanger, ghost_exchange.hpp:96-128,
+ * update_ghost_values / compress ghost_exchange.cpp:300-398) ---------------
+ * Pack, in-place ghost receives, compress and the ascending-rank
+ * accumulation run on the device over a transport: NCCL send/recv between
+ * the GPUs of one box (one process per GPU), or an in-process loopback
+ * (R rank operators in one process -- one host thread per rank calling
+ * dgx_apply -- whose messages become cudaMemcpyAsync between the ranks'
+ * device buffers; the reference's run_ranks + in-process queues,
+ * ghost_exchange.cpp:409-430). dgx_apply with an exchanger's hooks
+ * overlaps the exchange with the inner cells: the ghost-coupled cells run
+ * on a high-priority stream as soon as the update lands and their
+ * contributions are sent back while the inner cells still run. */
 typedef struct dgx_exchanger dgx_exchanger;
+typedef struct dgx_loopback dgx_loopback;
 dgx_status dgx_nccl_unique_id(void *id128);
 dgx_status dgx_exchanger_create(dgx_op *op, const void *nccl_id128,
                                 dgx_exchanger **ex);
+dgx_status dgx_loopback_create(int n_ranks, dgx_loopback **world);
+dgx_status dgx_loopback_destroy(dgx_loopback *world);
+dgx_status dgx_exchanger_create_loopback(dgx_op *op, dgx_loopback *world,
+                                         dgx_exchanger **ex);
 dgx_status dgx_exchanger_hooks(dgx_exchanger *ex, dgx_hooks *hooks);
 dgx_status dgx_exchanger_destroy(dgx_exchanger *ex);
 

@@ -6,15 +6,15 @@ kernels for sm_100a. There is no CPU fallback.
 """
 from ._lib import (DgxCudaError, DgxError, DgxInvalidArgument, DgxLogicError,
                    DgxRuntimeError)
-from .operators import (BASIS_KINDS, FACE_DTYPE, INVALID_CELL, DoFLayout, Geometry, Mesh,
-                        NcclExchanger, OperatorConfig, Partition, RankOperator,
+from .operators import (BASIS_KINDS, FACE_DTYPE, INVALID_CELL, DoFLayout, Geometry,
+                        LoopbackExchanger, LoopbackWorld, Mesh, NcclExchanger, OperatorConfig, Partition, RankOperator,
                         assign_face_owners, enumerate_faces, make_box_mesh,
                         make_operator_config, nccl_unique_id, partition_cells, random_vector)
 
 __all__ = [
     "DgxCudaError", "DgxError", "DgxInvalidArgument", "DgxLogicError",
     "DgxRuntimeError", "BASIS_KINDS", "FACE_DTYPE", "INVALID_CELL", "DoFLayout", "Geometry",
-    "Mesh", "NcclExchanger", "OperatorConfig", "Partition", "RankOperator",
+    "LoopbackExchanger", "LoopbackWorld", "Mesh", "NcclExchanger", "OperatorConfig", "Partition", "RankOperator",
     "assign_face_owners", "enumerate_faces", "make_box_mesh", "make_operator_config", "nccl_unique_id",
     "partition_cells", "random_vector",
 ]

@@ -115,6 +115,7 @@ EXPORTS = [
     "dgx_apply_phase", "dgx_accumulate_plan", "dgx_conjugate_gradient",
     "dgx_get_quadrature_points", "dgx_assemble_rhs", "dgx_set_velocity", "dgx_nccl_unique_id",
     "dgx_exchanger_create", "dgx_exchanger_hooks", "dgx_exchanger_destroy",
+    "dgx_loopback_create", "dgx_loopback_destroy", "dgx_exchanger_create_loopback",
     "dgx_get_geometry", "dgx_get_tasks", "dgx_get_stats", "dgx_random_uniform",
 ]
 

@@ -86,6 +86,11 @@ dgx::Operator &op_of(const dgx_op *op)
 }
 } // namespace
 
+namespace dgx
+{
+void set_last_error(const char *msg) { g_err = msg ? msg : ""; }
+} // namespace dgx
+
 extern "C" {
 
 const char *dgx_last_error(void) { return g_err.c_str(); }
@@ -293,8 +298,44 @@ dgx_status dgx_exchanger_create(dgx_op *op, const void *id128, dgx_exchanger **e
 {
   return guard([&] {
     dgx::Operator &o = op_of(op);
+    if (!id128 || !ex)
+      dgx::fail(dgx::Code::invalid_argument, "dgx_exchanger_create: null argument");
     auto e = std::make_unique<dgx_exchanger>();
-    e->impl = std::make_unique<dgx::Exchanger>(&o, id128, o.n_ranks());
+    e->impl = std::make_unique<dgx::Exchanger>(
+      &o, dgx::make_nccl_transport(id128, o.n_ranks(), o.layout().rank));
+    *ex = e.release();
+  });
+}
+
+struct dgx_loopback
+{
+  std::shared_ptr<dgx::LoopbackWorld> world;
+};
+
+dgx_status dgx_loopback_create(int n_ranks, dgx_loopback **world)
+{
+  return guard([&] {
+    if (!world)
+      dgx::fail(dgx::Code::invalid_argument, "dgx_loopback_create: null argument");
+    auto w = std::make_unique<dgx_loopback>();
+    w->world = dgx::make_loopback_world(n_ranks);
+    *world = w.release();
+  });
+}
+
+dgx_status dgx_loopback_destroy(dgx_loopback *world)
+{
+  return guard([&] { delete world; });
+}
+
+dgx_status dgx_exchanger_create_loopback(dgx_op *op, dgx_loopback *world, dgx_exchanger **ex)
+{
+  return guard([&] {
+    dgx::Operator &o = op_of(op);
+    if (!world || !ex)
+      dgx::fail(dgx::Code::invalid_argument, "dgx_exchanger_create_loopback: null argument");
+    auto e = std::make_unique<dgx_exchanger>();
+    e->impl = std::make_unique<dgx::Exchanger>(&o, dgx::make_loopback_transport(world->world, o.layout().rank));
     *ex = e.release();
   });
 }

@@ -154,6 +154,13 @@ void launch_scatter_values(T *dst, const long long *index, long long n, const T 
 template <typename T>
 void launch_scatter_add_values(T *dst, const long long *index, long long n, const T *src,
                                cudaStream_t s);
+// whole-cell plans: cell slot lists (value i = dof i % nq of cell i / nq)
+template <typename T>
+void launch_gather_cells(const T *src, const int *slot, long long n_cells, int nq, T *dst,
+                         cudaStream_t s);
+template <typename T>
+void launch_scatter_add_cells(T *dst, const int *slot, long long n_cells, int nq, const T *src,
+                              cudaStream_t s);
 template <typename Real>
 void launch_convert(const double *src, Real *dst, long long n, cudaStream_t s);
 

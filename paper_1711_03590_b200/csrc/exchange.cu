@@ -40,6 +40,35 @@ __global__ void scatter_add_values_kernel(T *__restrict__ dst, const long long *
     dst[index[i]] += src[i];
 }
 
+// Whole-cell plans (nodal / generic bases: every plan ships complete cells,
+// ghost_exchange.cpp:100-144): the plan is a list of cell slots, and value i
+// of the packed message is dof i % nq of cell i / nq -- 4 index bytes per
+// cell instead of 8 per value; consecutive threads touch consecutive dofs.
+template <typename T>
+__global__ void gather_cells_kernel(const T *__restrict__ src, const int *__restrict__ slot,
+                                    long long n, int nq, T *__restrict__ dst)
+{
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    {
+      const long long c = i / nq;
+      dst[i] = src[(long long)slot[c] * nq + (i - c * nq)];
+    }
+}
+
+// dst[cells of ONE neighbour plan] += src (no repeated cell inside a plan)
+template <typename T>
+__global__ void scatter_add_cells_kernel(T *__restrict__ dst, const int *__restrict__ slot,
+                                         long long n, int nq, const T *__restrict__ src)
+{
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    {
+      const long long c = i / nq;
+      dst[(long long)slot[c] * nq + (i - c * nq)] += src[i];
+    }
+}
+
 template <typename Real>
 __global__ void convert_kernel(const double *__restrict__ src, Real *__restrict__ dst,
                                long long n)
@@ -88,6 +117,28 @@ void launch_scatter_add_values(T *dst, const long long *index, long long n, cons
   cuda_check(cudaGetLastError(), "scatter_add_values");
 }
 
+template <typename T>
+void launch_gather_cells(const T *src, const int *slot, long long n_cells, int nq, T *dst,
+                         cudaStream_t s)
+{
+  const long long n = n_cells * nq;
+  if (n <= 0)
+    return;
+  gather_cells_kernel<<<grid_for(n), 256, 0, s>>>(src, slot, n, nq, dst);
+  cuda_check(cudaGetLastError(), "gather_cells");
+}
+
+template <typename T>
+void launch_scatter_add_cells(T *dst, const int *slot, long long n_cells, int nq, const T *src,
+                              cudaStream_t s)
+{
+  const long long n = n_cells * nq;
+  if (n <= 0)
+    return;
+  scatter_add_cells_kernel<<<grid_for(n), 256, 0, s>>>(dst, slot, n, nq, src);
+  cuda_check(cudaGetLastError(), "scatter_add_cells");
+}
+
 template <typename Real>
 void launch_convert(const double *src, Real *dst, long long n, cudaStream_t s)
 {
@@ -103,7 +154,11 @@ void launch_convert(const double *src, Real *dst, long long n, cudaStream_t s)
   template void launch_scatter_values<T>(T *, const long long *, long long, const T *,    \
                                          cudaStream_t);                                   \
   template void launch_scatter_add_values<T>(T *, const long long *, long long, const T *, \
-                                             cudaStream_t);
+                                             cudaStream_t);                               \
+  template void launch_gather_cells<T>(const T *, const int *, long long, int, T *,        \
+                                       cudaStream_t);                                     \
+  template void launch_scatter_add_cells<T>(T *, const int *, long long, int, const T *,   \
+                                            cudaStream_t);
 DGX_INST(double)
 DGX_INST(float)
 #undef DGX_INST

@@ -1,6 +1,7 @@
 // Rank operator: setup (layout, cell tasks, device geometry) and apply.
 // Mirrors RankOperator / OperatorImpl (reference operators.cpp:89-264).
 #include "operator.hpp"
+#include "nccl_exchange.hpp"
 
 #include "sipg_params.hpp"
 
@@ -338,6 +339,20 @@ void Operator::build_tasks(const std::vector<RawFace> &faces, const Partition &p
       send_index_.upload(si);
       recv_index_.upload(ri);
     }
+  // whole-cell send plans as cell slot lists (pack / accumulate per cell)
+  send_cell_offsets_.assign(1, 0);
+  if (layout_.whole_cells)
+    {
+      std::vector<int> sc;
+      for (const NeighborPlan &np : layout_.send)
+        {
+          for (std::uint32_t c : np.cells)
+            sc.push_back(static_cast<int>(layout_.slot(c)));
+          send_cell_offsets_.push_back((long long)sc.size());
+        }
+      if (!host_only_)
+        send_slots_.upload(sc);
+    }
 }
 
 void Operator::build_geometry(const dgx_setup &s, const std::vector<RawFace> &faces)
@@ -645,7 +660,8 @@ void Operator::launch_tasks(const int *tslot, const int *tgeo, const int2 *tface
   launch_apply<Real>(d_, k_, basis_, compressed_, prm, s);
 }
 
-void Operator::apply_phase(int phase, const void *u, void *y, cudaStream_t s, bool fp32)
+// argument checks of an apply (operators.cpp:220-222 checks before any hook)
+void Operator::check_apply_args(const void *u, const void *y, bool fp32) const
 {
   if (fp32 != (precision_ == 1))
     fail(Code::invalid_argument, "apply: precision does not match the operator config");
@@ -653,6 +669,11 @@ void Operator::apply_phase(int phase, const void *u, void *y, cudaStream_t s, bo
     fail(Code::invalid_argument, "apply: operator was created host-only (device < 0)");
   if (u == y)
     fail(Code::invalid_argument, "apply: source and destination must differ");
+}
+
+void Operator::apply_phase(int phase, const void *u, void *y, cudaStream_t s, bool fp32)
+{
+  check_apply_args(u, y, fp32);
   cuda_check(cudaSetDevice(device_), "cudaSetDevice");
   const int b = phase == 1 ? 0 : n_inner_;
   const int n = phase == 1 ? n_inner_ : n_coupled_;
@@ -673,7 +694,28 @@ void Operator::apply_phase(int phase, const void *u, void *y, cudaStream_t s, bo
 // RankOperator::apply (operators.cpp:217-264) with the exchange hooks.
 void Operator::apply(void *u, void *y, const dgx_hooks *hooks, cudaStream_t s, bool fp32)
 {
+  // every argument error is raised before a hook posts any communication
+  // (a failing apply must not leave the exchanger in flight)
+  check_apply_args(u, y, fp32);
   const bool have_ghosts = !layout_.ghosts.empty();
+  if (Exchanger *ex = native_exchanger(hooks); ex && ex->op() == this && n_coupled_ > 0)
+    {
+      // The native exchanger takes compress off the critical path: the
+      // ghost-coupled tasks run first on a high-priority stream as soon as
+      // the update has landed, their ghost contributions leave while the
+      // inner tasks still run on the caller's stream, and only the
+      // accumulation waits for both (same hooks, same results: the phases
+      // write disjoint cells, the accumulation order is unchanged).
+      cuda_check(cudaSetDevice(device_), "cudaSetDevice");
+      cudaStream_t sg = ghost_stream();
+      ex->start_update(u, s);
+      ex->finish_update(u, sg);
+      apply_phase(2, u, y, sg, fp32);
+      ex->compress_post(y, sg);
+      apply_phase(1, u, y, s, fp32);
+      ex->compress_finish(y, s);
+      return;
+    }
   auto call = [&](dgx_hook_fn fn, void *v, const char *what) {
     const dgx_status st = fn(hooks->ctx, v, static_cast<void *>(s));
     if (st != DGX_OK)
@@ -697,8 +739,25 @@ void Operator::apply(void *u, void *y, const dgx_hooks *hooks, cudaStream_t s, b
     call(hooks->compress, y, "compress");
 }
 
+cudaStream_t Operator::ghost_stream()
+{
+  if (!ghost_stream_)
+    {
+      int lo = 0, hi = 0;
+      cuda_check(cudaDeviceGetStreamPriorityRange(&lo, &hi), "cudaDeviceGetStreamPriorityRange");
+      cuda_check(cudaStreamCreateWithPriority(&ghost_stream_, cudaStreamNonBlocking, hi),
+                 "cudaStreamCreateWithPriority");
+    }
+  return ghost_stream_;
+}
+
 Operator::~Operator()
 {
+  if (ghost_stream_)
+    {
+      cudaSetDevice(device_);
+      cudaStreamDestroy(ghost_stream_);
+    }
   if (pipe_.sh || pipe_.sc || pipe_.sd)
     {
       cudaSetDevice(device_);

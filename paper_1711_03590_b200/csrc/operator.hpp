@@ -24,6 +24,7 @@ public:
   void apply(void *u, void *y, const dgx_hooks *hooks, cudaStream_t stream, bool fp32);
   // phase 1: inner tasks; phase 2: ghost-coupled + ghost-side tasks
   void apply_phase(int phase, const void *u, void *y, cudaStream_t stream, bool fp32);
+  void check_apply_args(const void *u, const void *y, bool fp32) const;
   void accumulate_plan(int idx, const double *contrib, double *y, cudaStream_t s);
   // y = A u with host buffers (dgx_apply_host): single-rank 3D layouts run a
   // z-slab pipeline (H2D of slab k+1, apply of slab k, D2H of slab k-1 on
@@ -67,6 +68,13 @@ public:
   const std::vector<long long> &recv_offsets() const { return recv_offsets_; }
   // whole ghost cells arrive in ghost storage order: receive in place
   bool recv_in_place() const { return recv_in_place_; }
+  // whole-cell plans: send cells as slot lists, per-plan offsets in cells
+  bool whole_cells() const { return layout_.whole_cells; }
+  const DeviceArray<int> &send_slots() const { return send_slots_; }
+  const std::vector<long long> &send_cell_offsets() const { return send_cell_offsets_; }
+  // the ghost-coupled phase of an exchanged apply runs on this stream
+  // (highest priority, created on first use), concurrent with phase 1
+  cudaStream_t ghost_stream();
 
 private:
   void build_tasks(const std::vector<RawFace> &faces, const Partition &part);
@@ -127,6 +135,9 @@ private:
   DeviceArray<long long> send_index_, recv_index_;
   std::vector<long long> send_offsets_, recv_offsets_; // in values, size plans+1
   bool recv_in_place_ = true;
+  DeviceArray<int> send_slots_;
+  std::vector<long long> send_cell_offsets_;
+  cudaStream_t ghost_stream_ = nullptr;
 };
 
 // solvers.cu

@@ -326,15 +326,23 @@ class RankOperator:
         layouts pipeline H2D / apply / D2H over z-slabs). u, y: numpy arrays
         or CPU torch tensors (pinned memory lets the copies overlap the
         apply); y is allocated when None. Returns y."""
-        def host_ptr(a):
+        def host_ptr(a, what):
             if isinstance(a, np.ndarray):
+                if not a.flags.c_contiguous:
+                    raise _lib.DgxInvalidArgument(f"apply_host: {what} must be C-contiguous")
                 return a.ctypes.data_as(C.c_void_p), a.size, a.dtype == np.float64
+            if not hasattr(a, "data_ptr"):
+                raise _lib.DgxInvalidArgument(f"apply_host: {what} must be a numpy array or a CPU tensor")
+            if getattr(a, "is_cuda", False) or str(getattr(a, "device", "cpu")) != "cpu":
+                raise _lib.DgxInvalidArgument(f"apply_host: {what} must be a host (CPU) buffer")
+            if not a.is_contiguous():
+                raise _lib.DgxInvalidArgument(f"apply_host: {what} must be contiguous")
             return C.c_void_p(a.data_ptr()), a.numel(), str(a.dtype) == "torch.float64"
         if isinstance(u, np.ndarray):
             u = np.ascontiguousarray(u, np.float64)
         if y is None:
             y = np.empty(self._layout.total_size) if isinstance(u, np.ndarray) else u.new_empty(u.shape)
-        (pu, nu, okd_u), (py, ny, okd_y) = host_ptr(u), host_ptr(y)
+        (pu, nu, okd_u), (py, ny, okd_y) = host_ptr(u, "u"), host_ptr(y, "y")
         if nu != self._layout.total_size or ny != self._layout.total_size:
             raise _lib.DgxInvalidArgument("apply: vector size mismatch")
         if not (okd_u and okd_y):
@@ -458,6 +466,7 @@ class NcclExchanger:
         buf = C.create_string_buffer(bytes(unique_id), 128)
         h = C.c_void_p()
         check(lib().dgx_exchanger_create(op._h, buf, C.byref(h)))
+        self._op = op  # the native exchanger uses the operator in every hook
         self._h = h
         self._hooks = _lib.CHooks()
         check(lib().dgx_exchanger_hooks(h, C.byref(self._hooks)))
@@ -470,6 +479,41 @@ class NcclExchanger:
         if h is not None and _lib._lib is not None:
             _lib._lib.dgx_exchanger_destroy(h)
             self._h = None
+
+
+class LoopbackWorld:
+    """In-process transport world for R rank operators (the reference's
+    run_ranks + in-process queues, ghost_exchange.cpp:409-430): each rank's
+    LoopbackExchanger turns its messages into cudaMemcpyAsync between the
+    ranks' device buffers. Run every rank's apply on its own host thread
+    (the C calls release the GIL)."""
+
+    def __init__(self, n_ranks: int):
+        h = C.c_void_p()
+        check(lib().dgx_loopback_create(C.c_int(n_ranks), C.byref(h)))
+        self._h = h
+        self.n_ranks = n_ranks
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and _lib._lib is not None:
+            _lib._lib.dgx_loopback_destroy(h)
+            self._h = None
+
+
+class LoopbackExchanger(NcclExchanger):
+    """The native device exchanger (the same pack / in-place receive /
+    compress / ascending-rank accumulation as NcclExchanger) over the
+    in-process loopback transport."""
+
+    def __init__(self, op: RankOperator, world: LoopbackWorld):
+        h = C.c_void_p()
+        check(lib().dgx_exchanger_create_loopback(op._h, world._h, C.byref(h)))
+        self._op = op
+        self._world = world  # the transport shares the world's mailboxes
+        self._h = h
+        self._hooks = _lib.CHooks()
+        check(lib().dgx_exchanger_hooks(h, C.byref(self._hooks)))
 
 
 def nccl_unique_id() -> bytes:

@@ -20,6 +20,23 @@ __global__ void dfma_kernel(double *out, int iters)
   out[blockIdx.x * blockDim.x + threadIdx.x] = s;
 }
 
+// FP32 FFMA peak (the fp32 roofline denominator of the c5f32 line)
+__global__ void ffma_kernel(float *out, int iters)
+{
+  float a[16];
+  for (int i = 0; i < 16; ++i)
+    a[i] = threadIdx.x * 1e-3f + i;
+  const float b = 1.0000001f, c = 1e-9f;
+  for (int it = 0; it < iters; ++it)
+#pragma unroll
+    for (int i = 0; i < 16; ++i)
+      a[i] = fmaf(a[i], b, c);
+  float s = 0;
+  for (int i = 0; i < 16; ++i)
+    s += a[i];
+  out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+}
+
 __device__ __forceinline__ void dmma(double &d0, double &d1, double a, double b)
 {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
@@ -101,8 +118,14 @@ int main()
       const double both_tf =
         (2.0 * 256 * warps * 4.0 * iters + 2.0 * blocks * threads * 8.0 * iters) /
         (ms * 1e-3) / 1e12;
-      std::printf("DFMA %.1f TFLOP/s  DMMA %.1f TFLOP/s  interleaved %.1f TFLOP/s\n", dfma_tf,
-                  dmma_tf, both_tf);
+      cudaEventRecord(e0);
+      ffma_kernel<<<blocks, threads>>>(reinterpret_cast<float *>(out), iters);
+      cudaEventRecord(e1);
+      cudaEventSynchronize(e1);
+      cudaEventElapsedTime(&ms, e0, e1);
+      const double ffma_tf = 2.0 * blocks * threads * 16.0 * iters / (ms * 1e-3) / 1e12;
+      std::printf("DFMA %.1f TFLOP/s  DMMA %.1f TFLOP/s  interleaved %.1f TFLOP/s  FFMA %.1f TFLOP/s\n",
+                  dfma_tf, dmma_tf, both_tf, ffma_tf);
     }
   return 0;
 }
