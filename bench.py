@@ -55,6 +55,16 @@ CONFIGS = {
     "c5h": (3, 160, 6, False, "cart", False, "fp64", 4,
             "C5h: 3D SIPG, Cartesian 160^3, p=6, affine, Hermite-like basis, fp64"),
 }
+# C4 at the paper's Table-4 size (BASELINE.json configs[3]'s "~56.6M DoFs" is
+# the 64^3 mesh): the size the reference arm can also run whole on the host
+CONFIGS["c4_64"] = (3, 64, 5, False, "vertex", True, "fp64", 3,
+                    "C4 at 64^3: 3D SIPG, deformed 64^3, p=5, a(x) folded, fp64 (56.6M DoFs)")
+# the BASELINE metric's 3D degree sweep p=3..8 (--degree): BASELINE vertex
+# deformation, per-q J^-T and JxW (g3), cells per direction chosen so the
+# mesh holds >= 1e8 DoFs (SWEEP_CELLS)
+CONFIGS["sweep"] = (3, 0, 5, False, "vertex", False, "fp64", 2,
+                    "3D degree sweep: SIPG, deformed n^3 (>= 1e8 DoFs), per-q J^-T and JxW, fp64")
+SWEEP_CELLS = {p: int(np.ceil((1e8 / (p + 1) ** 3) ** (1 / 3))) for p in range(1, 11)}
 # the paper's other operator on the C4 workload size (reference mesh
 # deformation, amplitude 0.05, mapping degree 2; constant transport field)
 CONFIGS["a4"] = (3, 128, 5, False, "mesh", False, "fp64", 3,
@@ -74,7 +84,10 @@ BASIS = {"c4h": "hermite_like", "c3h": "hermite_like", "c5h": "hermite_like"}
 # reference counter flops per DoF of C2 (2D, 256^2, Dirichlet) by degree
 C2_FLOPS_PER_DOF = {1: 76.00, 2: 74.67, 3: 86.00, 4: 90.24, 5: 100.00, 6: 105.80, 7: 115.00,
                     8: 121.48, 9: 130.40, 10: 137.26}
-REF_FLOPS_PER_DOF = {"c4": 240.0, "c3": 215.52, "c5": 260.82, "c5f32": 260.82,
+# 3D reference counter flops per DoF by degree (alpha / k^3 of the reference
+# counters, tiled cell path + faces; exact for any mesh)
+SWEEP_FLOPS_PER_DOF = {3: 198.0, 4: 215.52, 5: 240.0, 6: 260.82, 7: 285.0, 8: 307.11}
+REF_FLOPS_PER_DOF = {"c4": 240.0, "c4_64": 240.0, "c3": 215.52, "c5": 260.82, "c5f32": 260.82,
                      "c1": 198.0, "c2": 105.80,
                      # Hermite-like: plain (not even-odd) S passes, same counters
                      "c4h": 268.0, "c3h": 242.4, "c5h": 293.14, "a4": 93.0,
@@ -90,14 +103,15 @@ def peaks():
         return 6650.0, "fallback"
 
 
-def fp64_peak():
-    """FP64 FMA-pipe peak measured by tools/fp64_pipes.cu (profiles/fp64_peak.json);
-    nominal B200 figure otherwise."""
+def fp64_peak(prec="fp64"):
+    """FP64 (DFMA) or FP32 (FFMA) pipe peak measured by tools/fp64_pipes.cu
+    (profiles/fp64_peak.json); nominal B200 figures otherwise."""
+    key, nominal = ("fp64_dfma_tflops", 37.0) if prec == "fp64" else ("fp32_ffma_tflops", 74.0)
     try:
         with open(os.path.join(ROOT, "profiles", "fp64_peak.json")) as f:
-            return float(json.load(f)["fp64_dfma_tflops"]), "measured (tools/fp64_pipes.cu)"
+            return float(json.load(f)[key]), "measured (tools/fp64_pipes.cu)"
     except Exception:
-        return 37.0, "nominal"
+        return nominal, "nominal"
 
 
 class ClockSampler:
@@ -106,12 +120,31 @@ class ClockSampler:
          "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
-    def __init__(self, index):
+    def __init__(self, index, load=None):
         self.index = index
         self.proc = None
         self.lines = []
+        self.bracket = []
+        # load(): enqueues (asynchronously) ~0.3 s of the same work, so that
+        # a one-shot query just before and just after a short timed region
+        # sees the clocks under this load (the 100 ms sampler never fires
+        # inside ms-scale regions)
+        self.load = load
+
+    def query_under_load(self):
+        if self.load is None:
+            return
+        try:
+            self.load()
+            out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                  "--format=csv,noheader,nounits"], capture_output=True,
+                                 text=True, timeout=20).stdout
+            self.bracket += [ln.strip() for ln in out.splitlines() if ln.strip()]
+        except Exception:
+            pass
 
     def __enter__(self):
+        self.query_under_load()
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
@@ -128,6 +161,7 @@ class ClockSampler:
             self.lines.append(line.strip())
 
     def __exit__(self, *a):
+        self.query_under_load()
         if self.proc:
             self.proc.terminate()
             try:
@@ -138,7 +172,9 @@ class ClockSampler:
     def summary(self):
         sm, mx, reasons = [], 0.0, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
+        during = len(self.lines)
+        lines = self.lines if during >= 3 else self.lines + self.bracket
+        for ln in lines:
             parts = [p.strip() for p in ln.split(",")]
             if len(parts) < 9:
                 continue
@@ -152,8 +188,12 @@ class ClockSampler:
                     reasons.add(nm)
         if not sm:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
-        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx,
-                "reasons": sorted(reasons), "samples": len(sm)}
+        out = {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx,
+               "reasons": sorted(reasons), "samples": len(sm)}
+        if during < 3:
+            out["window"] = (f"{during} sample(s) inside the timed region + {len(self.bracket)} "
+                             "taken under the same load just before and after it")
+        return out
 
 
 def dist_env():
@@ -170,14 +210,17 @@ class RefBench:
     configuration at a reduced cell count, all host cores as threaded
     ranks, the better lane width of W in {4, 8}."""
 
-    def __init__(self, cfg_name, sample_cells=None):
+    def __init__(self, cfg_name, sample_cells=None, degree=None):
         from oracle import oracle as O
         from oracle import reflib as R
         d, n, p, periodic, kind, coef, prec, seed, label = CONFIGS[cfg_name]
+        if degree:
+            p = degree
         cores = os.cpu_count() or 1
         if sample_cells is None:
             sample_cells = {3: 16, 2: 128}[d]
         cells = [sample_cells] * d
+        self.cells = cells
         self.n_ranks = min(cores, int(np.prod(cells)))
         geo = None
         if kind == "vertex":
@@ -205,7 +248,7 @@ class RefBench:
         # applies per timed step: >= 0.5 s of CPU work (run_benchmark times
         # ceil(0.02 s / est) applies per repetition, bench.cpp:309-319)
         self.inner = max(1, int(np.ceil(0.5 / max(t1, 1e-6))))
-        self.sample = (f"{label.split(':')[0]} shape at {sample_cells}^{d} cells "
+        self.sample = (f"{label.split(':')[0]} shape (p={p}) at {sample_cells}^{d} cells "
                        f"({self.n_dofs} DoFs), reference RankOperator::apply, "
                        f"{BASIS.get(cfg_name, 'lagrange_gauss_lobatto')} basis, "
                        f"W={self.W}, R={self.n_ranks} threaded ranks (run_ranks + "
@@ -232,38 +275,63 @@ def main():
                     help="override the polynomial degree (C2 degree sweep p=1..10)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--weak", action="store_true",
+                    help="weak scaling: n x n x (n * N) cells over N GPUs (z-slabs of n^3 each)")
+    ap.add_argument("--ref-cells", type=int, default=None,
+                    help="cells per direction of the reference CPU sample (default 16 in 3D)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
     ws, rank, local = dist_env()
     d, n, p, periodic, kind, coef, prec, seed, label = CONFIGS[args.config]
-    if args.cells:
-        n = args.cells
     p_config = p
     if args.degree:
         p = args.degree
-    n_dofs = n ** d * (p + 1) ** d
+    if args.config == "sweep":
+        n = SWEEP_CELLS[p]
+        p_config = None
+        label = label.replace("n^3", f"{n}^3").replace("3D degree sweep", f"3D degree sweep p={p}")
+    if args.cells:
+        n = args.cells
+    cells = [n] * d
+    if args.weak:
+        cells[-1] = n * ws
+        label += f" (weak scaling: {n}^{d} cells per GPU)"
+    n_dofs = int(np.prod(cells)) * (p + 1) ** d
     metric = ("DG advection apply throughput (DoFs/s)" if ADVECTION.get(args.config)
               else "DG Laplacian apply throughput (DoFs/s)")
-    config = {"workload": label, "cells": [n] * d, "degree": p, "n_dofs": n_dofs,
+    config = {"workload": label, "cells": cells, "degree": p, "n_dofs": n_dofs,
               "basis": BASIS.get(args.config, "lagrange_gauss_lobatto"),
               "geometry_variant": VARIANT.get(args.config, "g3"),
               "seed": seed, "partition": f"contiguous lexicographic slabs x{args.gpus}",
               "l2": "inputs larger than L2 (no flush)"}
 
+    scaling = "weak" if args.weak else "strong"
     if args.impl == "reference":
         if rank != 0:
             return
-        rb = RefBench(args.config)
+        rb = RefBench(args.config, sample_cells=args.ref_cells, degree=p)
         for _ in range(args.warmup):
             rb.step()
-        val = statistics.median(rb.step() for _ in range(args.steps))
+        # one step = rb.inner applies of the sample; ms_per_step is the
+        # measured wall time of such a step (median), value its DoF rate
+        step_s = []
+        for _ in range(args.steps):
+            t0 = time.perf_counter()
+            rb.world.time(rb.inner)
+            step_s.append(time.perf_counter() - t0)
+        t_step = statistics.median(step_s)
+        val = rb.n_dofs * rb.inner / t_step
         info = {"cores": rb.n_ranks, "sample": rb.sample}
         out = {"metric": metric, "value": val, "unit": "DoF/s", "impl": "reference",
                "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
-               "ms_per_step": n_dofs / val * 1e3, "higher_is_better": True,
-               "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+               "ms_per_step": t_step * 1e3, "higher_is_better": True,
+               "scaling": scaling, "vs_baseline": None, "dtype": "f64", "data": "synthetic",
                "config": config,
+               "measured": {"cells": rb.cells, "n_dofs": rb.n_dofs, "applies_per_step": rb.inner,
+                            "note": "the reference CPU apply on a bounded sample of the workload "
+                                    "(same configuration, measured cell count above); value is "
+                                    "its DoF/s, ms_per_step the measured wall time of one step"},
                "cpu_baseline": {"value": val, "unit": "DoF/s", "cores": info["cores"],
                                 "kind": "reference", "sample": info["sample"]},
                "e2e": {"value": val, "unit": "DoF/s", "h2d_bytes_per_step": 0,
@@ -278,11 +346,14 @@ def main():
 
     torch.cuda.set_device(local)
     if ws > 1:
+        # NCCL's INIT log (ranks, transports, NVLS) stays visible to the driver
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
     t_setup = time.time()
-    mesh = (dgx.make_box_mesh(d, n, 0.05, periodic, 2) if kind == "mesh"
-            else dgx.make_box_mesh(d, n, 0.0, periodic, 1))
+    mesh = (dgx.make_box_mesh(d, cells, 0.05, periodic, 2) if kind == "mesh"
+            else dgx.make_box_mesh(d, cells, 0.0, periodic, 1))
     faces = dgx.enumerate_faces(mesh)
     part = dgx.partition_cells(mesh, ws)
     dgx.assign_face_owners(mesh, faces, part)
@@ -338,7 +409,18 @@ def main():
         flush = torch.empty(FLUSH_BYTES // 4, dtype=torch.float32, device=f"cuda:{local}")
         config["l2"] = (f"L2 flushed between timed steps (working set "
                         f"{work_bytes / 1e6:.0f} MB < 2x L2)")
-    with ClockSampler(local) as clk:
+    def load():  # ~0.3 s of the same applies, enqueued asynchronously
+        n_load = max(1, int(300.0 / max(first_ms, 1e-3)))
+        for _ in range(min(n_load, 2000)):
+            step()
+
+    ev_a, ev_b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev_a.record(stream)
+    step()
+    ev_b.record(stream)
+    ev_b.synchronize()
+    first_ms = ev_a.elapsed_time(ev_b)
+    with ClockSampler(local, load=load if first_ms * args.steps < 1000.0 else None) as clk:
         barrier()
         if flush is None:
             ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -427,16 +509,17 @@ def main():
             traffic = None
     # the binding resource: HBM bytes vs FP64 flops (reference counter flops,
     # SURVEY.md s.8d), whichever takes longer at its peak
-    fpk, fpk_kind = fp64_peak()
+    fpk, fpk_kind = fp64_peak(prec)
     ref_fpd = REF_FLOPS_PER_DOF.get(args.config, 0.0)
-    if p != p_config:  # degree override: C2's reference counter values per degree
-        ref_fpd = C2_FLOPS_PER_DOF.get(p, 0.0) if args.config == "c2" else 0.0
+    if p != p_config:  # degree override: the reference counter values per degree
+        ref_fpd = (C2_FLOPS_PER_DOF.get(p, 0.0) if args.config == "c2"
+                   else SWEEP_FLOPS_PER_DOF.get(p, 0.0) if d == 3 else 0.0)
     flops = ref_fpd * lay.owned_size
     t_hbm = alg_bytes / (hbm * 1e9)
     t_fp64 = flops / (fpk * 1e12)
-    if t_fp64 > t_hbm and prec == "fp64":
+    if t_fp64 > t_hbm:
         achieved_f = flops / (launch_ms * 1e-3) / 1e12
-        roofline = {"bound": "fp64", "achieved": achieved_f, "peak": fpk, "unit": "TFLOP/s",
+        roofline = {"bound": prec, "achieved": achieved_f, "peak": fpk, "unit": "TFLOP/s",
                     "frac": achieved_f / fpk, "traffic": traffic, "peak_source": fpk_kind,
                     "algorithmic_flops_per_launch": flops,
                     "hbm_achieved_gbs": achieved, "hbm_frac": achieved / hbm}
@@ -451,7 +534,7 @@ def main():
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
         try:
-            rb = RefBench(args.config)
+            rb = RefBench(args.config, sample_cells=args.ref_cells, degree=p)
             cpu = {"value": rb.rate(), "unit": "DoF/s", "cores": rb.n_ranks,
                    "kind": "reference", "sample": rb.sample + ", median of 11 steps"}
         except Exception as ex:  # reported, never silently replaced
@@ -461,7 +544,7 @@ def main():
     if rank == 0:
         out = {"metric": metric, "value": value, "unit": "DoF/s", "n_gpus": ws,
                "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
-               "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+               "higher_is_better": True, "scaling": scaling, "vs_baseline": None,
                "dtype": "f32" if prec == "fp32" else "f64", "data": "synthetic",
                "config": config, "e2e": e2e,
                "gpu_launches": int(args.steps * st["kernel_launches_per_apply"] +

@@ -453,6 +453,20 @@ class RankOperator:
                                      out.ctypes.data_as(C.c_void_p), C.byref(n)))
         return out
 
+    def tasks(self):
+        """The device task list in launch order: (slot, geometry record, face
+        entries [n_tasks, 2d, 2] = (neighbour slot | -1 boundary | -2 not
+        computed, face record | own side << 30), n_inner)."""
+        n, ni = C.c_int64(), C.c_int64()
+        check(lib().dgx_get_tasks(self._h, C.byref(n), C.byref(ni), None, None, None))
+        d = self.config.d
+        slot = np.empty(n.value, np.int32)
+        geo = np.empty(n.value, np.int32)
+        face = np.empty((n.value, 2 * d, 2), np.int32)
+        check(lib().dgx_get_tasks(self._h, C.byref(n), C.byref(ni), slot.ctypes.data_as(C.c_void_p),
+                                  geo.ctypes.data_as(C.c_void_p), face.ctypes.data_as(C.c_void_p)))
+        return slot, geo, face, int(ni.value)
+
     def stats(self) -> dict:
         st = _lib.CStats()
         check(lib().dgx_get_stats(self._h, C.byref(st)))
