@@ -97,7 +97,8 @@ class CStats(C.Structure):
                 ("bytes_vectors", C.c_double),
                 ("bytes_cell_geometry", C.c_double),
                 ("bytes_face_geometry", C.c_double),
-                ("cells_per_cta", C.c_int), ("threads_per_cta", C.c_int)]
+                ("cells_per_cta", C.c_int), ("threads_per_cta", C.c_int),
+                ("cartesian", C.c_int)]
 
 
 class CSolveReport(C.Structure):

@@ -95,7 +95,7 @@ struct AdvParams;
 // sipg.cu (kernels in sipg_gl.cu / sipg_gauss.cu / sipg_hermite.cu);
 // basis: 0 lagrange_gauss_lobatto, 1 lagrange_gauss, 2 hermite_like
 void upload_tables(int K, int basis);
-int kernel_cells_per_cta(int D, int K);
+int kernel_cells_per_cta(int D, int K, bool cart = false);
 // brick size of the pencil-pair kernel's CTAs (0: none; 4: 2x2x1; 8: 2x2x2)
 int kernel_brick(int D, int K);
 template <typename Real>
@@ -163,5 +163,8 @@ void launch_scatter_add_cells(T *dst, const int *slot, long long n_cells, int nq
                               cudaStream_t s);
 template <typename Real>
 void launch_convert(const double *src, Real *dst, long long n, cudaStream_t s);
+// compressed g3 records that are not axis-aligned (0: Operator::cart_)
+long long count_non_axis_records(int d, const double *cell_geo, long long n_cells, const double *face_geo,
+                                 const signed char *face_axis, long long n_faces);
 
 } // namespace dgx

@@ -78,6 +78,45 @@ __global__ void convert_kernel(const double *__restrict__ src, Real *__restrict_
     dst[i] = static_cast<Real>(src[i]);
 }
 
+// axis-aligned affine records (Operator::cart_): count the compressed cell
+// records with an off-diagonal J^{-T} entry above 1e-13 of the diagonal and
+// the compressed face records with an n.J^{-T} component off the face axis
+// above 1e-13 of the axis one (a box mesh's mapping Jacobian carries
+// round-off of ~1e-17 there: the sums of +-x_s/4 over the support points)
+__global__ void count_non_axis_kernel(int d, const double *__restrict__ cg, long long n_cells,
+                                      const double *__restrict__ fg, const signed char *__restrict__ axis,
+                                      long long n_faces, unsigned long long *bad)
+{
+  unsigned long long mine = 0;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n_cells + n_faces; i += stride)
+    {
+      constexpr double tol = 1e-13;
+      if (i < n_cells)
+        {
+          const double *r = cg + i * (d * d + 1);
+          double dmax = 0.0;
+          for (int a = 0; a < d; ++a)
+            dmax = fmax(dmax, fabs(r[a * d + a]));
+          for (int a = 0; a < d; ++a)
+            for (int b = 0; b < d; ++b)
+              if (a != b && !(fabs(r[a * d + b]) <= tol * dmax))
+                ++mine;
+        }
+      else
+        {
+          const long long f = i - n_cells;
+          const double *r = fg + f * (2 * d + 1);
+          const double ni = fabs(r[1 + axis[f]]), ne = fabs(r[1 + d + axis[f]]);
+          for (int b = 0; b < d; ++b)
+            if (b != axis[f] && !(fabs(r[1 + b]) <= tol * ni && fabs(r[1 + d + b]) <= tol * ne))
+              ++mine;
+        }
+    }
+  if (mine)
+    atomicAdd(bad, mine);
+}
+
 unsigned grid_for(long long n)
 {
   long long g = (n + 255) / 256;
@@ -137,6 +176,20 @@ void launch_scatter_add_cells(T *dst, const int *slot, long long n_cells, int nq
     return;
   scatter_add_cells_kernel<<<grid_for(n), 256, 0, s>>>(dst, slot, n, nq, src);
   cuda_check(cudaGetLastError(), "scatter_add_cells");
+}
+
+long long count_non_axis_records(int d, const double *cell_geo, long long n_cells, const double *face_geo,
+                                 const signed char *face_axis, long long n_faces)
+{
+  DeviceArray<unsigned long long> bad(1);
+  cuda_check(cudaMemset(bad.get(), 0, sizeof(unsigned long long)), "memset");
+  if (n_cells + n_faces > 0)
+    count_non_axis_kernel<<<grid_for(n_cells + n_faces), 256>>>(d, cell_geo, n_cells, face_geo, face_axis,
+                                                                 n_faces, bad.get());
+  cuda_check(cudaGetLastError(), "count_non_axis");
+  unsigned long long h = 0;
+  cuda_check(cudaMemcpy(&h, bad.get(), sizeof h, cudaMemcpyDeviceToHost), "count_non_axis");
+  return (long long)h;
 }
 
 template <typename Real>

@@ -568,6 +568,19 @@ void Operator::build_geometry(const dgx_setup &s, const std::vector<RawFace> &fa
         }
       run_geometry(job, nullptr);
     }
+  // axis-aligned affine records (every Cartesian box mesh): the CART
+  // kernels skip the tangential face terms, which are exact zeros here
+  cart_ = false;
+  if (compressed_ && kind_ == 0 && !sym_ && !host_only_ && !std::getenv("DGX_NO_CART"))
+    {
+      std::vector<signed char> ax(nmy);
+      for (long long i = 0; i < nmy; ++i)
+        ax[i] = static_cast<signed char>(faces[layout_.my_faces[i]].interior_face_number / 2);
+      DeviceArray<signed char> dax;
+      dax.upload(ax);
+      cuda_check(cudaDeviceSynchronize(), "geometry setup");
+      cart_ = count_non_axis_records(d_, cell_geo_.get(), n_owned, face_geo_.get(), dax.get(), nmy) == 0;
+    }
   if (precision_ == 1)
     {
       cell_geo_f_.resize(cell_geo_.size());
@@ -657,6 +670,7 @@ void Operator::launch_tasks(const int *tslot, const int *tgeo, const int2 *tface
   prm.n_owned = static_cast<int>(layout_.n_owned);
   prm.sym = sym_ ? 1 : 0;
   prm.ahead = 0;
+  prm.cart = cart_ ? 1 : 0;
   launch_apply<Real>(d_, k_, basis_, compressed_, prm, s);
 }
 
@@ -1030,7 +1044,8 @@ dgx_stats Operator::stats() const
   st.bytes_cell_geometry = es * (double)(kind_ == 1 ? adv_cell_.size() : cell_geo_.size());
   st.bytes_face_geometry =
     es * (double)(kind_ == 1 ? adv_face_.size() : face_geo_.size() + penalty_.size());
-  st.cells_per_cta = kernel_cells_per_cta(d_, k_);
+  st.cells_per_cta = kernel_cells_per_cta(d_, k_, cart_);
+  st.cartesian = cart_ ? 1 : 0;
   long long P = nq_ / k_;
   st.threads_per_cta = static_cast<int>(st.cells_per_cta * P);
   return st;

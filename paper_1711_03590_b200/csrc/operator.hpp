@@ -43,6 +43,7 @@ public:
   int n_ranks() const { return n_ranks_; }
   long long nq() const { return nq_; }
   bool compressed() const { return compressed_; }
+  bool cartesian_records() const { return cart_; }
   bool host_only() const { return host_only_; }
   // task lists as built on the host: slot, geometry record, 2d face entries
   const std::vector<int> &host_task_slot() const { return host_task_slot_; }
@@ -111,6 +112,7 @@ private:
   long long nq_ = 0, nqf_ = 0;
   RankLayout layout_;
   bool compressed_ = false;
+  bool cart_ = false; // compressed records axis-aligned (CART kernels)
   bool host_only_ = false;
   std::vector<int> host_task_slot_, host_task_geo_;
   std::vector<int2> host_task_face_;

@@ -33,11 +33,13 @@ void upload_tables(int K, int basis)
     }
 }
 
-int kernel_cells_per_cta(int D, int K)
+int kernel_cells_per_cta(int D, int K, bool cart)
 {
 #define DGX_NC(DD, KK)                                                                     \
   if (D == DD && K == KK)                                                                  \
-    return (DD == 3 && KK % 2 == 0) ? dev::PL<KK>::NC : dev::KernelShape<DD, KK, true>::NC;
+    return (DD == 3 && KK % 2 == 0) ? dev::PL<KK>::NC                                      \
+           : cart                    ? dev::KernelShape<DD, KK, true, true>::NC            \
+                                     : dev::KernelShape<DD, KK, true>::NC;
   DGX_NC(2, 2) DGX_NC(2, 3) DGX_NC(2, 4) DGX_NC(2, 5) DGX_NC(2, 6) DGX_NC(2, 7)
   DGX_NC(2, 8) DGX_NC(2, 9) DGX_NC(2, 10) DGX_NC(2, 11)
   DGX_NC(3, 2) DGX_NC(3, 3) DGX_NC(3, 4) DGX_NC(3, 5) DGX_NC(3, 6) DGX_NC(3, 7)

@@ -30,11 +30,11 @@ __device__ __forceinline__ void ldg_pair(const Real *un, int p, int m, Real &a, 
 // The neighbour pencils through face point p of both faces of axis A
 // (nodal bases), fetched one phase early (across the forward pass's last
 // barrier for axis 0, during the previous axis's test-side passes otherwise)
-template <typename Real, int D, int K, int A>
+template <typename Real, int D, int K, int A, bool CART = false>
 __device__ __forceinline__ void nb_fetch_v4(const ApplyParams<Real> &prm, const Real *cell, bool active, int p,
                                             Real (&x)[2][K])
 {
-  using L = SL<D, K>;
+  using L = SL<D, K, CART>;
   constexpr int NQ = L::NQ;
   int2 tf[2] = {make_int2(-2, 0), make_int2(-2, 0)};
   if (active)
@@ -328,6 +328,147 @@ __device__ __forceinline__ void face_axis_v4(const ApplyParams<Real> &prm, Real 
   // reads val/G, disjoint from OUT/DT used above, and its own barrier orders
   // everything after it; the quadrature-point phase that follows the last
   // axis writes only G and is followed by a barrier before OUT is read
+}
+
+// Both faces of axis A on axis-aligned affine records (CART: J^{-T}
+// diagonal and constant per cell, n.J^{-T} = (0, .., j_A, .., 0) per face,
+// verified at setup to 1e-13 relative: a box mesh's Jacobian carries
+// off-axis round-off of ~1e-17). The general phase above multiplies the
+// tangential derivatives and tangential test components by these (near)
+// zeros; here they are skipped: dn = j_A g_A on each side
+// (operators.cpp:977-1003, 1069-1089 without the off-axis terms), so only
+// the value and normal-derivative traces of the neighbour are interpolated
+// (two S passes each) and the test side is w = rv, rg_A = g j_A (no
+// tangential Dco^T passes). Results differ from the general path by the
+// dropped round-off terms (relative ~1e-16), far inside the 1e-12 parity
+// tolerance.
+template <typename Real, int D, int K, int A, bool HERM, bool GLN, typename HOOK>
+__device__ __forceinline__ void face_axis_cart(const ApplyParams<Real> &prm, Real *cell, bool active, int p,
+                                               Real wf, Real sp, const Real (&xnb)[2][K], HOOK &&after_flux)
+{
+  using L = SL<D, K, true>;
+  using T = TabLayout<K>;
+  constexpr int NQ = L::NQ, FP = L::FP, NL = L::NL, FS = L::FS;
+  const Real *val = cell;
+  const Real *G = cell + L::OFF_G;
+  Real *NB = cell + L::OFF_NB;  // face s: nu (2s), nw (2s+1)
+  Real *OUT = cell + L::OFF_OUT + (2 * A) * 2 * FP; // face s: w (2s), rgn (2s+1)
+  const int fp = fpt<D, K>(p);
+
+  int2 tf[2] = {make_int2(-2, 0), make_int2(-2, 0)};
+  if (active)
+    {
+      const int2 *tfs = reinterpret_cast<const int2 *>(cell + L::OFF_TF);
+      tf[0] = tfs[2 * A];
+      tf[1] = tfs[2 * A + 1];
+    }
+  Real jxw[2], tau[2], jo[2], jb[2];
+#pragma unroll
+  for (int s = 0; s < 2; ++s)
+    {
+      jxw[s] = tau[s] = jo[s] = jb[s] = Real(0);
+      if (tf[s].x != -2)
+        {
+          const int fid = tf[s].y & 0x3fffffff;
+          const int side = (tf[s].y >> 30) & 1;
+          const Real *fg = prm.face_geo + (long long)fid * (2 * D + 1);
+          jxw[s] = __ldg(fg) * wf;
+          jo[s] = __ldg(fg + 1 + side * D + A);
+          jb[s] = __ldg(fg + 1 + (1 - side) * D + A);
+          tau[s] = __ldg(prm.penalty + fid);
+        }
+    }
+  // own value and normal-gradient traces (rf rows along the normal)
+  Real own_u[2], own_g[2];
+  {
+    Real x[K];
+    load_pencil<Real, D, K, A>(val, p, x);
+    own_u[0] = dot_row<Real, K, T::oRf>(x);
+    own_u[1] = dot_row<Real, K, T::oRf + K>(x);
+    load_pencil<Real, D, K, A>(G + A * FS, p, x);
+    own_g[0] = dot_row<Real, K, T::oRf>(x);
+    own_g[1] = dot_row<Real, K, T::oRf + K>(x);
+  }
+  if constexpr (HERM)
+    {
+      Real xe[2], xi[2];
+#pragma unroll
+      for (int s = 0; s < 2; ++s)
+        {
+          xe[s] = xi[s] = Real(0);
+          if (tf[s].x >= 0)
+            {
+              const Real *un = prm.u + (long long)tf[s].x * NQ;
+              if (s == 0)
+                ldg_pair<Real, D, K, A>(un, p, K - 2, xi[s], xe[s]);
+              else
+                ldg_pair<Real, D, K, A>(un, p, 0, xe[s], xi[s]);
+            }
+        }
+#pragma unroll
+      for (int s = 0; s < 2; ++s)
+        {
+          const int me = s == 0 ? K - 1 : 0, mi = s == 0 ? K - 2 : 1;
+          const int ro = s == 0 ? K : 0;
+          const Real ve = xe[s] * (sp * hsign<Real, K>(me));
+          const Real vi = xi[s] * (sp * hsign<Real, K>(mi));
+          NB[(2 * s) * FP + fp] =
+            tab<Real, K>(T::oSf + ro + me) * ve + tab<Real, K>(T::oSf + ro + mi) * vi;
+          NB[(2 * s + 1) * FP + fp] =
+            tab<Real, K>(T::oDf + ro + me) * ve + tab<Real, K>(T::oDf + ro + mi) * vi;
+        }
+    }
+  else
+    {
+      const Real(&x)[2][K] = xnb;
+      NB[fp] = GLN ? x[0][K - 1] : dot_row<Real, K, T::oSf + K>(x[0]);
+      NB[FP + fp] = dot_row<Real, K, T::oDf + K>(x[0]);
+      NB[2 * FP + fp] = GLN ? x[1][0] : dot_row<Real, K, T::oSf>(x[1]);
+      NB[3 * FP + fp] = dot_row<Real, K, T::oDf>(x[1]);
+    }
+  __syncthreads();
+  // neighbour value / normal derivative to the face Gauss points: S along
+  // every tangential direction (face_eval's sweeps, operators.cpp:835-858)
+  if constexpr (D == 3)
+    {
+      for (int t = p; t < 4 * NL; t += L::P)
+        line_op<Real, D, K, 1, 0>(NB + (t / NL) * FP, nullptr, t % NL);
+      __syncthreads();
+    }
+  for (int t = p; t < 4 * NL; t += L::P)
+    line_op<Real, D, K, 0, 0>(NB + (t / NL) * FP, nullptr, t % NL);
+  __syncthreads();
+#pragma unroll
+  for (int s = 0; s < 2; ++s)
+    {
+      Real rv = Real(0), g = Real(0);
+      if (tf[s].x != -2)
+        {
+          const int side = (tf[s].y >> 30) & 1;
+          const Real dn_own = own_g[s] * jo[s];
+          if (tf[s].x == -1)
+            {
+              rv = (own_u[s] * tau[s] * Real(2) - dn_own) * jxw[s];
+              g = -(own_u[s] * jxw[s]);
+            }
+          else
+            {
+              const Real nu = NB[(2 * s) * FP + fp], nw = NB[(2 * s + 1) * FP + fp];
+              const Real dn_nb = nw * jb[s];
+              const Real sgn = side == 0 ? Real(1) : Real(-1);
+              const Real delta = own_u[s] - nu;
+              rv = (delta * tau[s] - sgn * ((dn_own + dn_nb) * Real(0.5))) * jxw[s];
+              g = -(sgn * delta * jxw[s] * Real(0.5));
+            }
+        }
+      OUT[(2 * s) * FP + fp] = rv;
+      OUT[(2 * s + 1) * FP + fp] = g * jo[s];
+    }
+  after_flux();
+  // no trailing barrier: the next axis's first writes are NB at this
+  // thread's own face point (read above by this thread only), and the
+  // quadrature-point phase after the last axis is followed by a barrier
+  // before OUT is read
 }
 
 } // namespace dev

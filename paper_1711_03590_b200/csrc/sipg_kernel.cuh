@@ -244,7 +244,10 @@ __device__ __forceinline__ unsigned ghost_layer_mask(const int2 *tf, int p)
 #define DGX_V4_W1 1
 #endif
 
-template <int D, int K>
+// CART: axis-aligned affine (Cartesian) records -- J^{-T} diagonal, face
+// normals n.J^{-T} along the face axis only (checked at setup): the face
+// phase needs no tangential derivatives (no DT fields, no W1 test fields)
+template <int D, int K, bool CART = false>
 struct SL
 {
   static constexpr int P = ipow_c(K, D - 1);
@@ -261,14 +264,14 @@ struct SL
   static constexpr int OFF_DT = OFF_NB + 4 * FP;      // 2(D-1) derivative fields
   // 2D int2 face entries (16 D bytes, fp32 or fp64); even offset so that
   // they stay 8-byte aligned in fp32 too
-  static constexpr int OFF_TF = (OFF_DT + 2 * (D - 1) * FP + 1) / 2 * 2;
+  static constexpr int OFF_TF = (OFF_DT + (CART ? 0 : 2 * (D - 1) * FP) + 1) / 2 * 2;
   static constexpr int SM_CELL = OFF_TF + 4 * D;
   // apply kernel, 3D: the t1 test parts Dco_t1^T rg_t1 (3 axes x 2 faces)
   // after the common layout, so that both test-side passes of a face axis
   // run in one phase (sipg_faces.cuh); the advection / rhs kernels do not
   // carry it
   static constexpr int OFF_W1 = (SM_CELL + 1) / 2 * 2;
-  static constexpr int SM_CELL_APPLY = OFF_W1 + (D == 3 && DGX_V4_W1 ? 6 * FP : 0);
+  static constexpr int SM_CELL_APPLY = OFF_W1 + (D == 3 && DGX_V4_W1 && !CART ? 6 * FP : 0);
 };
 
 // index of the m-th entry along axis A of pencil p (remaining axes
@@ -316,21 +319,27 @@ __device__ __forceinline__ int fln(int l, int m)
     return l + SL<D, K>::FK * m;
 }
 
-template <int D, int K, bool APPLY = false>
+template <int D, int K, bool APPLY = false, bool CART = false>
 struct KernelShape
 {
-  using L = SL<D, K>;
+  using L = SL<D, K, CART>;
   static constexpr int P = L::P;
   static constexpr int NQ = L::NQ;
   static constexpr int SM_CELL = APPLY ? L::SM_CELL_APPLY : L::SM_CELL;
   // ~160-256 threads per CTA and <= 74 KB of fp64 shared memory, so that
   // three CTAs share one SM (228 KB)
   static constexpr int NC_THREADS = (192 / P) > 0 ? 192 / P : 1;
-  static constexpr int NC_SMEM = (74 * 1024 / 8) / SM_CELL > 0 ? (74 * 1024 / 8) / SM_CELL : 1;
+  // CART cells are smaller: four CTAs per SM (4 x 55 KB)
+  static constexpr int SMEM_CAP = (CART ? 55 : 74) * 1024 / 8;
+  static constexpr int NC_SMEM = SMEM_CAP / SM_CELL > 0 ? SMEM_CAP / SM_CELL : 1;
   static constexpr int NC = NC_THREADS < NC_SMEM ? NC_THREADS : NC_SMEM;
   static constexpr int THREADS = NC * P;
   static constexpr int SMEM_REALS = NC * SM_CELL;
-  static constexpr int MIN_BLOCKS = (D == 2 && K >= 7) ? 2 : ((65536 / (THREADS * 3)) >= 96 ? 3 : 2);
+  static constexpr int MIN_BLOCKS =
+    (D == 2 && K >= 7) ? 2
+                       : ((CART && 65536 / (THREADS * 4) >= 96 && 4 * SMEM_REALS * 8 + 4096 <= 228 * 1024)
+                            ? 4
+                            : ((65536 / (THREADS * 3)) >= 96 ? 3 : 2));
 };
 
 template <typename Real, int D, int K, int A>
@@ -411,10 +420,10 @@ __device__ __forceinline__ void line_op(Real *x, Real *y, int l)
 // Backward step along axis A: v (pencil) += rf_s w_s + (Dco^T rf_s) rgn_s
 // for both faces of the axis (the transposed own traces, folded as rank-1
 // updates into the pass that already holds the pencil).
-template <typename Real, int D, int K, int A, bool USE_W1 = false>
+template <typename Real, int D, int K, int A, bool USE_W1 = false, bool CART = false>
 __device__ __forceinline__ void add_face_terms(const Real *cell, int p, Real (&v)[K])
 {
-  using L = SL<D, K>;
+  using L = SL<D, K, CART>;
   using T = TabLayout<K>;
   constexpr int FP = L::FP;
   const Real *OUT = cell + L::OFF_OUT + (2 * A) * 2 * FP;
@@ -446,12 +455,13 @@ namespace dev
 // that the instantiations of the per-basis translation units (each with its
 // own constant tables) are distinct kernels, not one weak host stub.
 // One task (cell slot) per group of P threads.
-template <typename Real, int D, int K, bool COMPRESSED, int BASIS>
+template <typename Real, int D, int K, bool COMPRESSED, int BASIS, bool CART = false>
 __device__ __forceinline__ void sipg_task(const ApplyParams<Real> &prm, Real *cell, int p,
                                           int task)
 {
   constexpr bool HERM = BASIS == 2;
-  using L = SL<D, K>;
+  static_assert(!CART || COMPRESSED, "CART records are compressed");
+  using L = SL<D, K, CART>;
   using T = TabLayout<K>;
   constexpr int P = L::P, NQ = L::NQ, FS = L::FS;
   const bool active = task < prm.n_tasks;
@@ -574,7 +584,7 @@ __device__ __forceinline__ void sipg_task(const ApplyParams<Real> &prm, Real *ce
   // neighbour pencils of the first face axis, in flight across the barrier
   Real xnb[2][K];
   if constexpr (!HERM)
-    nb_fetch_v4<Real, D, K, 0>(prm, cell, active, p, xnb);
+    nb_fetch_v4<Real, D, K, 0, CART>(prm, cell, active, p, xnb);
   __syncthreads();
 
   // ---- faces ------------------------------------------------------------
@@ -598,16 +608,32 @@ __device__ __forceinline__ void sipg_task(const ApplyParams<Real> &prm, Real *ce
             wf *= wa;
           }
       }
-    face_axis_v4<Real, D, K, 0, COMPRESSED, HERM, BASIS == 0>(prm, cell, task, active, p, wf, sp, xnb, [&] {
-      if constexpr (!HERM)
-        nb_fetch_v4<Real, D, K, 1>(prm, cell, active, p, xnb);
-    });
-    face_axis_v4<Real, D, K, 1, COMPRESSED, HERM, BASIS == 0>(prm, cell, task, active, p, wf, sp, xnb, [&] {
-      if constexpr (!HERM && D == 3)
-        nb_fetch_v4<Real, D, K, 2>(prm, cell, active, p, xnb);
-    });
-    if constexpr (D == 3)
-      face_axis_v4<Real, D, K, 2, COMPRESSED, HERM, BASIS == 0>(prm, cell, task, active, p, wf, sp, xnb, [] {});
+    if constexpr (CART)
+      {
+        face_axis_cart<Real, D, K, 0, HERM, BASIS == 0>(prm, cell, active, p, wf, sp, xnb, [&] {
+          if constexpr (!HERM)
+            nb_fetch_v4<Real, D, K, 1, CART>(prm, cell, active, p, xnb);
+        });
+        face_axis_cart<Real, D, K, 1, HERM, BASIS == 0>(prm, cell, active, p, wf, sp, xnb, [&] {
+          if constexpr (!HERM && D == 3)
+            nb_fetch_v4<Real, D, K, 2, CART>(prm, cell, active, p, xnb);
+        });
+        if constexpr (D == 3)
+          face_axis_cart<Real, D, K, 2, HERM, BASIS == 0>(prm, cell, active, p, wf, sp, xnb, [] {});
+      }
+    else
+      {
+        face_axis_v4<Real, D, K, 0, COMPRESSED, HERM, BASIS == 0>(prm, cell, task, active, p, wf, sp, xnb, [&] {
+          if constexpr (!HERM)
+            nb_fetch_v4<Real, D, K, 1>(prm, cell, active, p, xnb);
+        });
+        face_axis_v4<Real, D, K, 1, COMPRESSED, HERM, BASIS == 0>(prm, cell, task, active, p, wf, sp, xnb, [&] {
+          if constexpr (!HERM && D == 3)
+            nb_fetch_v4<Real, D, K, 2>(prm, cell, active, p, xnb);
+        });
+        if constexpr (D == 3)
+          face_axis_v4<Real, D, K, 2, COMPRESSED, HERM, BASIS == 0>(prm, cell, task, active, p, wf, sp, xnb, [] {});
+      }
   }
 #else
   {
@@ -733,23 +759,34 @@ __device__ __forceinline__ void sipg_task(const ApplyParams<Real> &prm, Real *ce
 #pragma unroll
             for (int b = 0; b < D; ++b)
               g[b] = G[b * FS + q];
-#pragma unroll
-            for (int i = 0; i < D; ++i)
+            if constexpr (CART)
               {
-                Real acc = jit[i * D] * g[0];
+                // diagonal J^{-T} (off-diagonal round-off <= 1e-13 relative, dropped)
+                (void)ph;
 #pragma unroll
-                for (int j = 1; j < D; ++j)
-                  acc += jit[i * D + j] * g[j];
-                ph[i] = acc;
+                for (int i = 0; i < D; ++i)
+                  t[i] = (jit[i * D + i] * (jit[i * D + i] * g[i])) * jw;
               }
-#pragma unroll
-            for (int i = 0; i < D; ++i)
+            else
               {
-                Real acc = jit[i] * ph[0];
 #pragma unroll
-                for (int j = 1; j < D; ++j)
-                  acc += jit[j * D + i] * ph[j];
-                t[i] = acc * jw;
+                for (int i = 0; i < D; ++i)
+                  {
+                    Real acc = jit[i * D] * g[0];
+#pragma unroll
+                    for (int j = 1; j < D; ++j)
+                      acc += jit[i * D + j] * g[j];
+                    ph[i] = acc;
+                  }
+#pragma unroll
+                for (int i = 0; i < D; ++i)
+                  {
+                    Real acc = jit[i] * ph[0];
+#pragma unroll
+                    for (int j = 1; j < D; ++j)
+                      acc += jit[j * D + i] * ph[j];
+                    t[i] = acc * jw;
+                  }
               }
           }
         else
@@ -768,7 +805,7 @@ __device__ __forceinline__ void sipg_task(const ApplyParams<Real> &prm, Real *ce
         // ---- backward, first pass (z): v = Dco_z^T t_2 + z-face terms
         Real v[K];
         apply_Dt<Real, K>(tz, v);
-        add_face_terms<Real, D, K, 2, true>(cell, p, v);
+        add_face_terms<Real, D, K, 2, !CART, CART>(cell, p, v);
         store_pencil<Real, D, K, 2>(val, p, v);
       }
   }
@@ -791,7 +828,7 @@ __device__ __forceinline__ void sipg_task(const ApplyParams<Real> &prm, Real *ce
         load_pencil<Real, D, K, 1>(G + FS, p, x);
         apply_Dt<Real, K>(x, v);
       }
-    add_face_terms<Real, D, K, 1, true>(cell, p, v);
+    add_face_terms<Real, D, K, 1, !CART, CART>(cell, p, v);
     store_pencil<Real, D, K, 1>(val, p, v);
     __syncthreads();
     load_pencil<Real, D, K, 0>(G, p, x);
@@ -800,7 +837,7 @@ __device__ __forceinline__ void sipg_task(const ApplyParams<Real> &prm, Real *ce
 #pragma unroll
     for (int m = 0; m < K; ++m)
       v[m] += z[m];
-    add_face_terms<Real, D, K, 0, true>(cell, p, v);
+    add_face_terms<Real, D, K, 0, !CART, CART>(cell, p, v);
     apply_St<Real, K>(v, z);
     store_pencil<Real, D, K, 0>(val, p, z);
     __syncthreads();
@@ -827,19 +864,19 @@ __device__ __forceinline__ void sipg_task(const ApplyParams<Real> &prm, Real *ce
   }
 }
 
-template <typename Real, int D, int K, bool COMPRESSED, int BASIS>
-__global__ void __launch_bounds__(KernelShape<D, K, true>::THREADS, KernelShape<D, K, true>::MIN_BLOCKS)
+template <typename Real, int D, int K, bool COMPRESSED, int BASIS, bool CART = false>
+__global__ void __launch_bounds__(KernelShape<D, K, true, CART>::THREADS, KernelShape<D, K, true, CART>::MIN_BLOCKS)
   sipg_apply_kernel(const ApplyParams<Real> prm)
 {
-  using KS = KernelShape<D, K, true>;
-  using L = SL<D, K>;
+  using KS = KernelShape<D, K, true, CART>;
+  using L = SL<D, K, CART>;
   constexpr int P = L::P, NC = KS::NC;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   Real *smem = reinterpret_cast<Real *>(smem_raw);
   const int lc = threadIdx.x / P;
   const int p = threadIdx.x - lc * P;
   Real *cell = smem + lc * KS::SM_CELL;
-  sipg_task<Real, D, K, COMPRESSED, BASIS>(prm, cell, p, blockIdx.x * NC + lc);
+  sipg_task<Real, D, K, COMPRESSED, BASIS, CART>(prm, cell, p, blockIdx.x * NC + lc);
 }
 
 } // namespace dev

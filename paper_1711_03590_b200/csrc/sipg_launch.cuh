@@ -140,17 +140,27 @@ void launch_pairs(const dev::ApplyParams<double> &prm, cudaStream_t s)
   cuda_check(cudaGetLastError(), "sipg_pairs_kernel launch");
 }
 
-template <typename Real, int D, int K, bool C>
+#ifndef DGX_CART_PAIRS
+#define DGX_CART_PAIRS 1 // even K, 3D fp64 Cartesian: 1 = the general pair kernel, 0 = the single-pencil CART kernel
+#endif
+
+template <typename Real, int D, int K, bool C, bool CART = false>
 void launch_one(const dev::ApplyParams<Real> &prm, cudaStream_t s)
 {
-  if constexpr (DGX_PAIRS && D == 3 && sizeof(Real) == 8 && (K % 2 == 0 || DGX_PAIRS_ODD))
+  if constexpr (C && !CART)
+    if (prm.cart && !(DGX_CART_PAIRS && DGX_PAIRS && D == 3 && sizeof(Real) == 8 && K % 2 == 0))
+      {
+        launch_one<Real, D, K, C, true>(prm, s);
+        return;
+      }
+  if constexpr (!CART && DGX_PAIRS && D == 3 && sizeof(Real) == 8 && (K % 2 == 0 || DGX_PAIRS_ODD))
     {
       launch_pairs<K, C>(prm, s);
       return;
     }
-  using KS = dev::KernelShape<D, K, true>;
+  using KS = dev::KernelShape<D, K, true, CART>;
   const size_t smem = (size_t)KS::SMEM_REALS * sizeof(Real);
-  auto kern = dev::sipg_apply_kernel<Real, D, K, C, DGX_BASIS>;
+  auto kern = dev::sipg_apply_kernel<Real, D, K, C, DGX_BASIS, CART>;
   static std::set<int> configured;
   int devid = 0;
   cuda_check(cudaGetDevice(&devid), "cudaGetDevice");

@@ -38,6 +38,15 @@
 #ifndef DGX_EXP_NO_META_PF
 #define DGX_EXP_NO_META_PF 0
 #endif
+// own value and normal-gradient traces of every face axis computed in the
+// forward pass, from the pencils the thread holds in registers there (val
+// along y after S_y, along x / z in the G_0 / G_2 steps, and the G_A output
+// of each): the face phase then loads only the two tangential gradient
+// fields along A (2 instead of 4 volume-field loads per axis); the x-face
+// points of a thread become its permuted x-pass pair (cx, wx)
+#ifndef DGX_PAIRS_FWDTRACE
+#define DGX_PAIRS_FWDTRACE 0
+#endif
 // neighbour trace along t0 as row dot products at the thread's own face
 // points, fused with the flux (no row pass, one barrier less per axis)
 #ifndef DGX_PAIRS_ROWDOT
@@ -72,6 +81,10 @@ struct PL
   // f-fastest column passes below are conflict-free)
   static constexpr int FP = K == 6 ? 36 : pr_stride(KP * K, H);
   static constexpr int OFF_G = FS;
+#ifdef DGX_EXP_PAIRS_NO_FACE_SMALL // ablation: cell integral only, no face storage at all
+  static constexpr int OFF_OUT = 4 * FS, OFF_W1 = OFF_OUT, OFF_NB = OFF_OUT, OFF_DT = OFF_OUT,
+                       OFF_RG1 = OFF_OUT, OFF_TF = OFF_OUT;
+#else
   static constexpr int OFF_OUT = 4 * FS;         // 3 axes x (w0, w1, rgn0, rgn1)
   // W1: the t1 part Dco_t1^T rg_t1 of the face test values, 3 axes x 2
   // faces, so that the row and column test passes run in one phase
@@ -80,6 +93,7 @@ struct PL
   static constexpr int OFF_DT = OFF_NB + 4 * FP;
   static constexpr int OFF_RG1 = OFF_DT + 4 * FP; // row-dot variant: rg along t1, 2 faces
   static constexpr int OFF_TF = OFF_RG1 + (DGX_PAIRS_ROWDOT ? 2 * FP : 0); // 6 int2 face entries
+#endif
   // threads per cell: P2 (option: rounded up to whole quarter-warps, so that
   // no quarter-warp mixes two cells; lanes >= P2 duplicate the last pair and
   // take line-operation tasks)
@@ -123,6 +137,15 @@ struct PL
   static constexpr int SMEM_REALS = NC * SM_CELL;
 };
 
+// timing ablation only (wrong results): face records / neighbour cells
+// remapped into a small window that stays cache-resident
+#ifdef DGX_EXP_FACE_RESIDENT
+#define DGX_EXP_FID(f) ((f) & 1023)
+#define DGX_EXP_NBSLOT(x) ((x) & 1023)
+#else
+#define DGX_EXP_FID(f) (f)
+#define DGX_EXP_NBSLOT(x) (x)
+#endif
 template <int K>
 __device__ __forceinline__ void pr_sync()
 {
@@ -131,6 +154,12 @@ __device__ __forceinline__ void pr_sync()
   else
     __syncthreads();
 }
+// timing ablation only (wrong results): face-phase barriers removed
+#ifdef DGX_EXP_NO_FACE_SYNC
+#define DGX_EXP_FSYNC() ((void)0)
+#else
+#define DGX_EXP_FSYNC() pr_sync<K>()
+#endif
 
 __device__ __forceinline__ double2 lds2(const double *p) { return *reinterpret_cast<const double2 *>(p); }
 __device__ __forceinline__ void sts2(double *p, double a, double b)
@@ -339,6 +368,9 @@ __device__ __forceinline__ unsigned pr_ghost_mask(const int2 *tf, int x, int y)
 template <int K, int A>
 __device__ __forceinline__ void pr_face_terms(const double *cell, int c, int w, double (&v)[2][K])
 {
+#ifdef DGX_EXP_PAIRS_NO_FACE_SMALL
+  return;
+#endif
   using L = PL<K>;
   using T = TabLayout<K>;
   const double *OUT = cell + L::OFF_OUT + (2 * A) * 2 * L::FP;
@@ -421,7 +453,7 @@ __device__ __forceinline__ void pr_nb_fetch(const ApplyParams<double> &prm, cons
   pr_axis_faces<K, A>(cell, active, lc, tf, inr, PNB);
 #pragma unroll
   for (int s = 0; s < 2; ++s)
-    pr_ldg_if<K, A>(tf[s].x >= 0 && !inr[s], prm.u + (long long)(tf[s].x >= 0 ? tf[s].x : 0) * PL<K>::NQ,
+    pr_ldg_if<K, A>(tf[s].x >= 0 && !inr[s], prm.u + (long long)DGX_EXP_NBSLOT(tf[s].x >= 0 ? tf[s].x : 0) * PL<K>::NQ,
                     c, w, x[s]);
 }
 
@@ -432,7 +464,7 @@ template <int K, int A, bool COMPRESSED, bool HERM, bool GLN, typename HOOK>
 __device__ __forceinline__ void pr_face_axis(const ApplyParams<double> &prm, double *cell, bool active,
                                              int c, int w, int t, int lc, const double (&wf)[2],
                                              const double (&sp)[2], const double (&xnb)[2][2][K],
-                                             HOOK &&before_wpass)
+                                             const double (&trc)[2][2][2], HOOK &&before_wpass)
 {
   using L = PL<K>;
   using T = TabLayout<K>;
@@ -466,7 +498,7 @@ __device__ __forceinline__ void pr_face_axis(const ApplyParams<double> &prm, dou
           jo[s][e][b] = 0.0;
       if (tf[s].x != -2)
         {
-          const int fid = tf[s].y & 0x3fffffff;
+          const int fid = DGX_EXP_FID(tf[s].y & 0x3fffffff);
           const int side = (tf[s].y >> 30) & 1;
           if constexpr (COMPRESSED)
             {
@@ -495,6 +527,17 @@ __device__ __forceinline__ void pr_face_axis(const ApplyParams<double> &prm, dou
   double own_u[2][2], own_g[2][2][3];
   {
     double x[2][K];
+#if DGX_PAIRS_FWDTRACE
+#pragma unroll
+    for (int s = 0; s < 2; ++s)
+#pragma unroll
+      for (int e = 0; e < 2; ++e)
+        {
+          own_u[s][e] = trc[s][e][0];
+          own_g[s][e][A] = trc[s][e][1];
+        }
+#else
+    (void)trc;
     pr_load<K, A>(val, c, w, x);
 #pragma unroll
     for (int e = 0; e < 2; ++e)
@@ -502,9 +545,12 @@ __device__ __forceinline__ void pr_face_axis(const ApplyParams<double> &prm, dou
         own_u[0][e] = dot_row<double, K, T::oRf>(x[e]);
         own_u[1][e] = dot_row<double, K, T::oRf + K>(x[e]);
       }
+#endif
 #pragma unroll
     for (int b = 0; b < 3; ++b)
       {
+        if (DGX_PAIRS_FWDTRACE && b == A)
+          continue;
         pr_load<K, A>(G + b * FS, c, w, x);
 #pragma unroll
         for (int e = 0; e < 2; ++e)
@@ -583,7 +629,7 @@ __device__ __forceinline__ void pr_face_axis(const ApplyParams<double> &prm, dou
           sts2(NB + (2 * s + 1) * FP + fp, dn_own[s][0], dn_own[s][1]);
         }
     }
-  pr_sync<K>();
+  DGX_EXP_FSYNC();
 
   // pass 1, along t1 (column pairs): nu -> (S nu, D nu -> DT[2+s]); nw -> S nw
   for (int tk = t; tk < 4 * H; tk += L::G)
@@ -617,7 +663,7 @@ __device__ __forceinline__ void pr_face_axis(const ApplyParams<double> &prm, dou
             sts2(dt + FK * m, y[0][m], y[1][m]);
         }
     }
-  pr_sync<K>();
+  DGX_EXP_FSYNC();
   // rest of the face geometry (L2-resident: prefetched at task start;
   // issued here so that pass 2 overlaps the latency)
   double jxw[2][2], tau[2], jb[2][2][3];
@@ -635,7 +681,7 @@ __device__ __forceinline__ void pr_face_axis(const ApplyParams<double> &prm, dou
         }
       if (tf[s].x != -2)
         {
-          const int fid = tf[s].y & 0x3fffffff;
+          const int fid = DGX_EXP_FID(tf[s].y & 0x3fffffff);
           const int side = (tf[s].y >> 30) & 1;
           if constexpr (COMPRESSED)
             {
@@ -698,7 +744,7 @@ __device__ __forceinline__ void pr_face_axis(const ApplyParams<double> &prm, dou
             sts2(dt + 2 * j, y[2 * j], 2 * j + 1 < K ? y[2 * j + 1] : 0.0);
         }
     }
-  pr_sync<K>();
+  DGX_EXP_FSYNC();
 #endif
 
   // flux at the two face points of both faces
@@ -808,7 +854,7 @@ __device__ __forceinline__ void pr_face_axis(const ApplyParams<double> &prm, dou
       sts2((DGX_PAIRS_ROWDOT ? cell + L::OFF_RG1 + s * FP : DT + (2 + s) * FP) + fp,
            g[0] * jo[s][0][A == 2 ? 1 : 2], g[1] * jo[s][1][A == 2 ? 1 : 2]);
     }
-  pr_sync<K>();
+  DGX_EXP_FSYNC();
   before_wpass();
   // w = rv + Dco_t0^T rg_t0 (rows) ... [W1: and the column tasks below in
   // the same phase, into W1]
@@ -967,8 +1013,18 @@ __global__ void __launch_bounds__(PL<K>::THREADS, PL<K>::MINB)
       // without it once the neighbour pencils are fetched one phase early)
     }
 
+  // face points of axis 0 (FWDTRACE: the permuted x-pass pair)
+  const int c0 = DGX_PAIRS_FWDTRACE ? cx : c, w0 = DGX_PAIRS_FWDTRACE ? wx : w;
+  // own traces per axis, [A][face s][pencil e][value, normal gradient]
+  double tr[3][2][2][2];
+  (void)tr;
   // Hermite-like: sign of the tangential indices of the two face points /
   // z-pencils (x = 2c + e, y = w), and the ghost layers of a ghost-side task
+  double sp0[2] = {1.0, 1.0};
+  if constexpr (HERM)
+#pragma unroll
+    for (int e = 0; e < 2; ++e)
+      sp0[e] = hsign<double, K>(2 * c0 + e) * hsign<double, K>(w0);
   double sp[2] = {1.0, 1.0};
   unsigned gmask[2] = {(1u << K) - 1u, (1u << K) - 1u};
   if constexpr (HERM)
@@ -1015,14 +1071,29 @@ __global__ void __launch_bounds__(PL<K>::THREADS, PL<K>::MINB)
       apply_S<double, K>(x[e], z[e]);
     pr_store<K, 2>(val, c, w, z);
     pr_sync<K>();
+#ifndef DGX_EXP_PAIRS_NO_FACE
     if constexpr (!HERM)
-      pr_nb_fetch<K, 0>(prm, cell, active, c, w, lc, xnb);
+      pr_nb_fetch<K, 0>(prm, cell, active, c0, w0, lc, xnb);
+#endif
     pr_load<K, 0>(val, cx, wx, x);
 #pragma unroll
     for (int e = 0; e < 2; ++e)
       apply_S<double, K>(x[e], z[e]);
     pr_store<K, 0>(val, cx, wx, z);
     pr_sync<K>();
+    // own value / normal-gradient traces of axis A from the pencils along A
+    // held here (val in v, G_A in g): rf rows (operators.cpp:794-858 own side)
+    auto traces = [&](int a, const double(&v)[2][K], const double(&g)[2][K]) {
+#pragma unroll
+      for (int e = 0; e < 2; ++e)
+        {
+          tr[a][0][e][0] = dot_row<double, K, T::oRf>(v[e]);
+          tr[a][1][e][0] = dot_row<double, K, T::oRf + K>(v[e]);
+          tr[a][0][e][1] = dot_row<double, K, T::oRf>(g[e]);
+          tr[a][1][e][1] = dot_row<double, K, T::oRf + K>(g[e]);
+        }
+    };
+    (void)traces;
     pr_load<K, 1>(val, c, w, x);
 #pragma unroll
     for (int e = 0; e < 2; ++e)
@@ -1032,17 +1103,23 @@ __global__ void __launch_bounds__(PL<K>::THREADS, PL<K>::MINB)
     for (int e = 0; e < 2; ++e)
       apply_D<double, K>(z[e], x[e]);
     pr_store<K, 1>(G + FS, c, w, x);
+    if constexpr (DGX_PAIRS_FWDTRACE)
+      traces(1, z, x);
     pr_sync<K>();
     pr_load<K, 0>(val, cx, wx, x);
 #pragma unroll
     for (int e = 0; e < 2; ++e)
       apply_D<double, K>(x[e], z[e]);
     pr_store<K, 0>(G, cx, wx, z);
+    if constexpr (DGX_PAIRS_FWDTRACE)
+      traces(0, x, z);
     pr_load<K, 2>(val, c, w, x);
 #pragma unroll
     for (int e = 0; e < 2; ++e)
       apply_D<double, K>(x[e], z[e]);
     pr_store<K, 2>(G + 2 * FS, c, w, z);
+    if constexpr (DGX_PAIRS_FWDTRACE)
+      traces(2, x, z);
   }
   pr_sync<K>();
 
@@ -1071,27 +1148,32 @@ __global__ void __launch_bounds__(PL<K>::THREADS, PL<K>::MINB)
   // ---- faces ------------------------------------------------------------
   {
     // tangential weight prod_t w[q_t] of the two face points (compressed)
-    double wf[2] = {1.0, 1.0};
+    double wf[2] = {1.0, 1.0}, wf0[2] = {1.0, 1.0};
     if constexpr (COMPRESSED)
       {
 #pragma unroll
         for (int e = 0; e < 2; ++e)
           {
-            const int q0 = 2 * c + e;
-            double wa = 0.0, wb = 0.0;
+            const int q0 = 2 * c + e, q00 = 2 * c0 + e;
+            double wa = 0.0, wb = 0.0, wa0 = 0.0, wb0 = 0.0;
 #pragma unroll
             for (int i = 0; i < K; ++i)
               {
                 wa = (q0 == i) ? tab<double, K>(T::oW + i) : wa;
                 wb = (w == i) ? tab<double, K>(T::oW + i) : wb;
+                wa0 = (q00 == i) ? tab<double, K>(T::oW + i) : wa0;
+                wb0 = (w0 == i) ? tab<double, K>(T::oW + i) : wb0;
               }
             wf[e] = (1.0 * wa) * wb;
+            wf0[e] = (1.0 * wa0) * wb0;
           }
       }
     auto none = [] {};
 #ifdef DGX_EXP_PAIRS_NO_FACE // ablation: cell integral only
+#ifndef DGX_EXP_PAIRS_NO_FACE_SMALL
     for (int i = t; i < 12 * L::FP; i += L::G)
       cell[L::OFF_OUT + i] = 0.0;
+#endif
     pr_sync<K>();
     (void)none;
     (void)wf;
@@ -1099,15 +1181,15 @@ __global__ void __launch_bounds__(PL<K>::THREADS, PL<K>::MINB)
     if (false)
 #endif
     {
-    pr_face_axis<K, 0, COMPRESSED, HERM, BASIS == 0>(prm, cell, active, c, w, t, lc, wf, sp, xnb, [&] {
+    pr_face_axis<K, 0, COMPRESSED, HERM, BASIS == 0>(prm, cell, active, c0, w0, t, lc, wf0, sp0, xnb, tr[0], [&] {
       if constexpr (!HERM)
         pr_nb_fetch<K, 1>(prm, cell, active, c, w, lc, xnb);
     });
-    pr_face_axis<K, 1, COMPRESSED, HERM, BASIS == 0>(prm, cell, active, c, w, t, lc, wf, sp, xnb, [&] {
+    pr_face_axis<K, 1, COMPRESSED, HERM, BASIS == 0>(prm, cell, active, c, w, t, lc, wf, sp, xnb, tr[1], [&] {
       if constexpr (!HERM)
         pr_nb_fetch<K, 2>(prm, cell, active, c, w, lc, xnb);
     });
-    pr_face_axis<K, 2, COMPRESSED, HERM, BASIS == 0>(prm, cell, active, c, w, t, lc, wf, sp, xnb, [&] {
+    pr_face_axis<K, 2, COMPRESSED, HERM, BASIS == 0>(prm, cell, active, c, w, t, lc, wf, sp, xnb, tr[2], [&] {
 #pragma unroll
       for (int m = 0; m < QD - 1; ++m)
         load_layer(m);

@@ -28,6 +28,7 @@ struct ApplyParams
   int n_owned; // slots >= n_owned are ghost cells (ghost-side tasks)
   int sym;     // 1: cell records hold the g4 coefficient [geo][d(d+1)/2][NQ]
   int ahead;   // tasks resident on the device at once (set by the launcher)
+  int cart;    // 1: axis-aligned affine records (Operator::cart_), CART kernels
 };
 
 // Advection apply (OperatorKind::advection, operators.cpp:634-667 cell,

@@ -274,3 +274,42 @@ def test_ny_beyond_one_tile(torch):
         ref = O.Problem(3, cells, p, deform=("vertex", 0.1), coefficient=True).apply(x)
         y = _device_apply(torch, op, x)
         assert rel_linf(y, ref) < TOL64 and rel_l2(y, ref) < TOL64
+
+
+@pytest.mark.parametrize("d,cells,p,periodic,basis", [
+    (3, [4, 5, 3], 6, False, "lagrange_gauss_lobatto"),   # C5 shape, odd k
+    (3, [3, 4, 5], 4, True, "lagrange_gauss_lobatto"),
+    (3, [3, 3, 4], 4, False, "hermite_like"),
+    (3, [3, 4, 3], 2, False, "lagrange_gauss"),
+    (2, [6, 5], 5, False, "lagrange_gauss_lobatto"),
+])
+@pytest.mark.parametrize("precision", ["fp64", "fp32"])
+def test_cart_kernel(torch, d, cells, p, periodic, basis, precision):
+    """Cartesian box meshes run the CART kernels (axis-aligned affine
+    records: the tangential face terms, products with round-off zeros, are
+    skipped): flagged in stats, equal to the general kernel (DGX_NO_CART)
+    to round-off and to the C restatement within the parity tolerance."""
+    import os
+    from oracle import oracle as O
+    D = _dgx()
+    mesh = D.make_box_mesh(d, cells, 0.0, periodic, 1)
+    faces = D.enumerate_faces(mesh)
+    part = D.partition_cells(mesh, 1)
+    D.assign_face_owners(mesh, faces, part)
+    cfg = D.OperatorConfig(d=d, p=p, basis=basis, precision=precision)
+    op = D.RankOperator(mesh, part, faces, D.Geometry(), cfg)
+    os.environ["DGX_NO_CART"] = "1"
+    try:
+        gen = D.RankOperator(mesh, part, faces, D.Geometry(), cfg)
+    finally:
+        del os.environ["DGX_NO_CART"]
+    assert op.stats()["cartesian"] == 1 and gen.stats()["cartesian"] == 0
+    x = D.random_vector(int(np.prod(cells)) * (p + 1) ** d, 9)
+    dt = torch.float32 if precision == "fp32" else torch.float64
+    y = _device_apply(torch, op, x, dt)
+    yg = _device_apply(torch, gen, x, dt)
+    b = {"lagrange_gauss_lobatto": 0, "lagrange_gauss": 1, "hermite_like": 2}[basis]
+    ref = O.Problem(d, cells, p, periodic=periodic, basis=b).apply(x)
+    tol = TOL32 if precision == "fp32" else TOL64
+    assert rel_linf(y, ref) < tol and rel_l2(y, ref) < tol
+    assert rel_linf(y, yg) < (1e-5 if precision == "fp32" else 1e-13)
