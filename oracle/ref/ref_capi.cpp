@@ -107,8 +107,16 @@ struct World
   std::shared_ptr<const GeometryCache> geom;
   std::vector<std::unique_ptr<RankOperator>> ops;
   std::vector<ExchangePlan> plans;
+  std::vector<DoFLayout> layouts; // topology-only worlds (no operators)
   bool external_geometry = false;
 };
+
+const DoFLayout &layout_of(const World &w, int rank)
+{
+  if (!w.layouts.empty())
+    return w.layouts.at(rank);
+  return w.ops.at(rank)->layout();
+}
 
 long long ipow(int b, int e)
 {
@@ -380,6 +388,26 @@ int dgref_world_create_ext(int d, const int *cells, int periodic, int p,
   });
 }
 
+// Topology only (no geometry, no operator): mesh, faces, partition, face
+// owners, every rank's DoFLayout (build_dof_layout, W = 1) and exchange
+// plans (build_exchange_plan) -- the bit-exact maps at sizes where the
+// geometry precompute would take an hour (dof_layout.cpp:170-253,
+// ghost_exchange.cpp:100-144, mesh.cpp:70-232).
+int dgref_topology_create(int d, const int *cells, int periodic, int p, int n_ranks, void **out)
+{
+  return guard([&] {
+    std::unique_ptr<World> w(make_world_common(d, cells, 0.0, 1, periodic, p, n_ranks, 1));
+    const FaceAccess access = make_basis(w->cfg.basis, w->cfg.p).face_access;
+    for (int r = 0; r < n_ranks; ++r)
+      {
+        w->layouts.push_back(build_dof_layout(w->mesh, w->partition, w->faces, r, w->cfg.k(), 1));
+        w->plans.push_back(build_exchange_plan(w->layouts.back(), w->faces, w->partition, access,
+                                               ghost_need(w->cfg.kind)));
+      }
+    *out = w.release();
+  });
+}
+
 void dgref_world_destroy(void *w) { delete static_cast<World *>(w); }
 
 // counts[0..7]: n_cells, n_faces, n_q_cell, n_q_face, compressed, dofs/cell,
@@ -390,10 +418,10 @@ int dgref_world_counts(void *wp, long long *counts)
     const World &w = *static_cast<World *>(wp);
     counts[0] = w.mesh.n_cells();
     counts[1] = static_cast<long long>(w.faces.size());
-    counts[2] = w.geom->n_q_cell;
-    counts[3] = w.geom->n_q_face;
-    counts[4] = w.geom->compressed() ? 1 : 0;
-    counts[5] = w.ops[0]->layout().dofs_per_cell;
+    counts[2] = w.geom ? w.geom->n_q_cell : 0;
+    counts[3] = w.geom ? w.geom->n_q_face : 0;
+    counts[4] = w.geom && w.geom->compressed() ? 1 : 0;
+    counts[5] = layout_of(w, 0).dofs_per_cell;
     counts[6] = w.partition.n_ranks;
     counts[7] = counts[0] * counts[5];
   });
@@ -455,7 +483,7 @@ int dgref_world_layout(void *wp, int rank, long long *info,
                        std::uint32_t *ghost_cells, int *ghost_owner)
 {
   return guard([&] {
-    const DoFLayout &l = static_cast<World *>(wp)->ops.at(rank)->layout();
+    const DoFLayout &l = layout_of(*static_cast<World *>(wp), rank);
     info[0] = l.owned_cell_begin;
     info[1] = l.n_owned_cells;
     info[2] = static_cast<long long>(l.ghost_global_cells.size());

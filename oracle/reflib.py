@@ -156,6 +156,27 @@ class World:
             lib().dgref_set_operator(C.c_int(0), None, C.c_int(0))
             lib().dgref_set_variant(C.c_int(3))
 
+    @classmethod
+    def topology(cls, d, cells, p, n_ranks, periodic=False, basis="gl"):
+        """Mesh, faces, partition, layouts and exchange plans only (no
+        geometry, no operators): the reference's maps at full sizes."""
+        self = cls.__new__(cls)
+        self.kind = "laplacian"
+        cells = list(cells) + [1] * (3 - len(cells))
+        cc = (C.c_int * 3)(*cells)
+        h = C.c_void_p()
+        self.d, self.p, self.k = d, p, p + 1
+        with _basis(basis):
+            _chk(lib().dgref_topology_create(C.c_int(d), cc, C.c_int(int(periodic)), C.c_int(p),
+                                             C.c_int(n_ranks), C.byref(h)))
+        self._h = h
+        c = (C.c_longlong * 8)()
+        _chk(lib().dgref_world_counts(h, c))
+        (self.n_cells, self.n_faces, self.n_q_cell, self.n_q_face,
+         self.compressed, self.dofs_per_cell, self.n_ranks,
+         self.n_dofs) = [int(x) for x in c]
+        return self
+
     def _create(self, d, cells, p, n_ranks, amplitude, mapping_degree, periodic, W,
                 geometry):
         cells = list(cells) + [1] * (3 - len(cells))

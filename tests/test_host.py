@@ -220,3 +220,45 @@ def test_large_topology_matches_oracle():
     for r in (0, 3, 6):
         op = dgx.RankOperator(mesh, part, faces, dgx.Geometry(), dgx.OperatorConfig(d=3, p=2), r, -1)
         assert np.array_equal(op.layout().ghost_global_cells, P.rank_ghosts(r))
+
+
+@pytest.mark.parametrize("R", [2, 4, 8])
+def test_c4_size_topology_matches_reference(R):
+    """The multi-GPU maps at the size bench.py --gpus N runs (C4: 128^3,
+    Dirichlet) against the reference's own functions, compiled unmodified
+    in oracle/_ref: enumerate_faces, partition_cells, assign_face_owners
+    (mesh.cpp:70-232), every rank's DoFLayout (build_dof_layout,
+    dof_layout.cpp:170-253) and exchange plans (build_exchange_plan,
+    ghost_exchange.cpp:100-144). Bit-exact. p = 1 keeps the reference's
+    per-cell index lists small; the cell sets do not depend on p."""
+    from oracle import reflib as R_
+    if not R_.available():
+        pytest.skip("oracle/_ref not built")
+    n, p = 128, 1
+    ref = R_.World.topology(3, [n] * 3, p, R)
+    fr = ref.faces()
+    mesh = dgx.make_box_mesh(3, [n] * 3, 0.0, False, 1)
+    faces = dgx.enumerate_faces(mesh)
+    assert np.array_equal(faces["interior_cell"], fr["interior"])
+    assert np.array_equal(faces["exterior_cell"], fr["exterior"])
+    assert np.array_equal(faces["interior_face_number"], fr["fn_int"])
+    assert np.array_equal(faces["exterior_face_number"], fr["fn_ext"])
+    part = dgx.partition_cells(mesh, R)
+    dgx.assign_face_owners(mesh, faces, part)
+    assert np.array_equal(part.cell_owner, fr["cell_owner"])
+    assert np.array_equal(part.face_owner, fr["face_owner"])
+    for r in range(R):
+        op = dgx.RankOperator(mesh, part, faces, dgx.Geometry(), dgx.OperatorConfig(d=3, p=p), r, -1)
+        lay, rl = op.layout(), ref.layout(r)
+        assert (lay.owned_cell_begin, lay.n_owned_cells, lay.owned_size, lay.total_size) == \
+            (rl["owned_cell_begin"], rl["n_owned_cells"], rl["owned_size"], rl["total_size"])
+        assert np.array_equal(lay.ghost_global_cells, rl["ghost_cells"])
+        assert np.array_equal(lay.ghost_owner, rl["ghost_owner"])
+        for which in ("send", "recv"):
+            mine, theirs = op.plans(which), ref.plans(r, which)
+            assert [nb for nb, _ in mine] == [q["neighbor"] for q in theirs]
+            for (nb, cells), (offs, dofs), q in zip(mine, op.plan_dofs(which), theirs):
+                assert np.array_equal(cells, q["cells"])
+                assert np.array_equal(offs, q["offsets"])
+                assert np.array_equal(dofs, q["dofs"])
+        del op
