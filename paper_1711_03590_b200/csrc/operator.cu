@@ -581,6 +581,9 @@ void Operator::build_geometry(const dgx_setup &s, const std::vector<RawFace> &fa
       cuda_check(cudaDeviceSynchronize(), "geometry setup");
       cart_ = count_non_axis_records(d_, cell_geo_.get(), n_owned, face_geo_.get(), dax.get(), nmy) == 0;
     }
+  // nodal bases: the tensor-product kernel (sipg_cart.cuh); the Hermite-like
+  // basis keeps the collocation CART kernels
+  tensor_ = cart_ && basis_ != 2 && !std::getenv("DGX_NO_TENSOR");
   if (precision_ == 1)
     {
       cell_geo_f_.resize(cell_geo_.size());
@@ -670,7 +673,7 @@ void Operator::launch_tasks(const int *tslot, const int *tgeo, const int2 *tface
   prm.n_owned = static_cast<int>(layout_.n_owned);
   prm.sym = sym_ ? 1 : 0;
   prm.ahead = 0;
-  prm.cart = cart_ ? 1 : 0;
+  prm.cart = cart_ ? (tensor_ ? 2 : 1) : 0;
   launch_apply<Real>(d_, k_, basis_, compressed_, prm, s);
 }
 
@@ -1044,9 +1047,17 @@ dgx_stats Operator::stats() const
   st.bytes_cell_geometry = es * (double)(kind_ == 1 ? adv_cell_.size() : cell_geo_.size());
   st.bytes_face_geometry =
     es * (double)(kind_ == 1 ? adv_face_.size() : face_geo_.size() + penalty_.size());
-  st.cells_per_cta = kernel_cells_per_cta(d_, k_, cart_);
-  st.cartesian = cart_ ? 1 : 0;
   long long P = nq_ / k_;
+  if (tensor_)
+    {
+      st.cells_per_cta = static_cast<int>(192 / P > 0 ? 192 / P : 1); // dev::CartShape
+      st.cartesian = 2;
+    }
+  else
+    {
+      st.cells_per_cta = kernel_cells_per_cta(d_, k_, cart_);
+      st.cartesian = cart_ ? 1 : 0;
+    }
   st.threads_per_cta = static_cast<int>(st.cells_per_cta * P);
   return st;
 }

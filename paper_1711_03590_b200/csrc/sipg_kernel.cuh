@@ -60,10 +60,14 @@ struct TabLayout
   static constexpr int oDnE = oRD + 2 * K;   // even-odd halves of the nodal D
   static constexpr int oDnO = oDnE + CE * CE;
   static constexpr int oDn = oDnO + CE * CE; // plain nodal D, K x K (Gauss point, node)
-  static constexpr int size = oDn + K * K;
+  // 1D mass M1 = S^T W S and stiffness K1 = D^T W D of the nodal basis with the
+  // k-point Gauss rule (even-odd halves): the tensor-product Cartesian kernel
+  static constexpr int oM1E = oDn + K * K, oM1O = oM1E + CE * CE;
+  static constexpr int oK1E = oM1O + CE * CE, oK1O = oK1E + CE * CE;
+  static constexpr int size = oK1O + CE * CE;
 };
 
-constexpr int tab_size(int K) { return 10 * ((K + 1) / 2) * ((K + 1) / 2) + 3 * K * K + 9 * K; }
+constexpr int tab_size(int K) { return 14 * ((K + 1) / 2) * ((K + 1) / 2) + 3 * K * K + 9 * K; }
 // offset of the table for K (K >= 2) inside the per-precision constant block
 constexpr int tab_offset(int K) { return K <= 2 ? 0 : tab_offset(K - 1) + tab_size(K - 1); }
 constexpr int kMaxK = 11;

@@ -8,6 +8,7 @@
 #include "setup.hpp"
 #include "sipg_kernel.cuh"
 #include "sipg_pairs.cuh"
+#include "sipg_cart.cuh"
 #include "sipg_rhs.cuh"
 #include "sipg_adv.cuh"
 
@@ -96,6 +97,19 @@ std::vector<double> build_table(int K)
   o += 2 * c2;
   for (int i = 0; i < K * K; ++i) // and plainly (row-dot neighbour traces, sipg_pairs.cuh)
     o[i] = t.D[i];
+  o += K * K;
+  // 1D mass and stiffness matrices of the k-point Gauss rule (sipg_cart.cuh)
+  std::vector<double> M1(K * K, 0.0), K1(K * K, 0.0);
+  for (int i = 0; i < K; ++i)
+    for (int j = 0; j < K; ++j)
+      for (int q = 0; q < K; ++q)
+        {
+          M1[i * K + j] += t.S[q * K + i] * t.qw[q] * t.S[q * K + j];
+          K1[i * K + j] += t.D[q * K + i] * t.qw[q] * t.D[q * K + j];
+        }
+  eo_halves(M1, K, o, o + c2);
+  o += 2 * c2;
+  eo_halves(K1, K, o, o + c2);
   return tab;
 }
 
@@ -116,7 +130,10 @@ template <int K, bool C>
 void launch_pairs(const dev::ApplyParams<double> &prm, cudaStream_t s)
 {
   using L = dev::PL<K>;
-  const size_t smem = (size_t)L::SMEM_REALS * sizeof(double);
+#ifndef DGX_EXP_SMEM_PAD
+#define DGX_EXP_SMEM_PAD 0 // occupancy ablation: unused extra shared memory per CTA
+#endif
+  const size_t smem = (size_t)L::SMEM_REALS * sizeof(double) + DGX_EXP_SMEM_PAD;
   auto kern = dev::sipg_pairs_kernel<K, C, DGX_BASIS>;
   static std::set<int> configured;
   set_smem_once(kern, smem, configured);
@@ -140,6 +157,27 @@ void launch_pairs(const dev::ApplyParams<double> &prm, cudaStream_t s)
   cuda_check(cudaGetLastError(), "sipg_pairs_kernel launch");
 }
 
+// Axis-aligned affine records, nodal bases: the tensor-product kernel
+// (sipg_cart.cuh); prm.cart == 2
+template <typename Real, int D, int K>
+void launch_cart(const dev::ApplyParams<Real> &prm, cudaStream_t s)
+{
+#if DGX_BASIS != 2
+  using CS = dev::CartShape<Real, D, K>;
+  const size_t smem = (size_t)CS::SMEM_REALS * sizeof(Real);
+  auto kern = dev::sipg_cart_kernel<Real, D, K, DGX_BASIS>;
+  static std::set<int> configured;
+  set_smem_once(kern, smem, configured);
+  const int grid = (prm.n_tasks + CS::NC - 1) / CS::NC;
+  if (grid > 0)
+    kern<<<grid, CS::THREADS, smem, s>>>(prm);
+  cuda_check(cudaGetLastError(), "sipg_cart_kernel launch");
+#else
+  (void)prm, (void)s;
+  fail(Code::logic_error, "sipg_cart_kernel: not built for the Hermite-like basis");
+#endif
+}
+
 #ifndef DGX_CART_PAIRS
 #define DGX_CART_PAIRS 1 // even K, 3D fp64 Cartesian: 1 = the general pair kernel, 0 = the single-pencil CART kernel
 #endif
@@ -147,6 +185,12 @@ void launch_pairs(const dev::ApplyParams<double> &prm, cudaStream_t s)
 template <typename Real, int D, int K, bool C, bool CART = false>
 void launch_one(const dev::ApplyParams<Real> &prm, cudaStream_t s)
 {
+  if constexpr (C && !CART && DGX_BASIS != 2)
+    if (prm.cart == 2)
+      {
+        launch_cart<Real, D, K>(prm, s);
+        return;
+      }
   if constexpr (C && !CART)
     if (prm.cart && !(DGX_CART_PAIRS && DGX_PAIRS && D == 3 && sizeof(Real) == 8 && K % 2 == 0))
       {

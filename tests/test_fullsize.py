@@ -285,9 +285,10 @@ def test_ny_beyond_one_tile(torch):
 ])
 @pytest.mark.parametrize("precision", ["fp64", "fp32"])
 def test_cart_kernel(torch, d, cells, p, periodic, basis, precision):
-    """Cartesian box meshes run the CART kernels (axis-aligned affine
-    records: the tangential face terms, products with round-off zeros, are
-    skipped): flagged in stats, equal to the general kernel (DGX_NO_CART)
+    """Cartesian box meshes run the tensor-product kernel (nodal bases) or the
+    collocation CART kernels (Hermite-like basis, DGX_NO_TENSOR; axis-aligned
+    affine records: the tangential face terms, products with round-off zeros,
+    are skipped): flagged in stats, equal to the general kernel (DGX_NO_CART)
     to round-off and to the C restatement within the parity tolerance."""
     import os
     from oracle import oracle as O
@@ -303,11 +304,21 @@ def test_cart_kernel(torch, d, cells, p, periodic, basis, precision):
         gen = D.RankOperator(mesh, part, faces, D.Geometry(), cfg)
     finally:
         del os.environ["DGX_NO_CART"]
-    assert op.stats()["cartesian"] == 1 and gen.stats()["cartesian"] == 0
+    os.environ["DGX_NO_TENSOR"] = "1"
+    try:
+        col = D.RankOperator(mesh, part, faces, D.Geometry(), cfg)
+    finally:
+        del os.environ["DGX_NO_TENSOR"]
+    # nodal bases: the tensor-product kernel (2); Hermite-like and DGX_NO_TENSOR: the
+    # collocation CART kernels (1)
+    assert op.stats()["cartesian"] == (1 if basis == "hermite_like" else 2)
+    assert col.stats()["cartesian"] == 1 and gen.stats()["cartesian"] == 0
     x = D.random_vector(int(np.prod(cells)) * (p + 1) ** d, 9)
     dt = torch.float32 if precision == "fp32" else torch.float64
     y = _device_apply(torch, op, x, dt)
     yg = _device_apply(torch, gen, x, dt)
+    yc = _device_apply(torch, col, x, dt)
+    assert rel_linf(yc, yg) < (1e-5 if precision == "fp32" else 1e-13)
     b = {"lagrange_gauss_lobatto": 0, "lagrange_gauss": 1, "hermite_like": 2}[basis]
     ref = O.Problem(d, cells, p, periodic=periodic, basis=b).apply(x)
     tol = TOL32 if precision == "fp32" else TOL64
