@@ -307,8 +307,8 @@ typedef struct dgx_stats
   int64_t kernel_launches_per_apply;
   double bytes_vectors, bytes_cell_geometry, bytes_face_geometry; /* per apply */
   int cells_per_cta, threads_per_cta;
-  int cartesian; /* axis-aligned affine records: 1 the collocation CART kernels run
-                    (Hermite-like basis), 2 the tensor-product kernel (nodal bases) */
+  int cartesian; /* axis-aligned affine records: 2 the tensor-product kernel runs,
+                    1 the collocation CART kernels (DGX_NO_TENSOR set at creation) */
 } dgx_stats;
 dgx_status dgx_get_stats(const dgx_op *op, dgx_stats *out);
 

@@ -581,9 +581,9 @@ void Operator::build_geometry(const dgx_setup &s, const std::vector<RawFace> &fa
       cuda_check(cudaDeviceSynchronize(), "geometry setup");
       cart_ = count_non_axis_records(d_, cell_geo_.get(), n_owned, face_geo_.get(), dax.get(), nmy) == 0;
     }
-  // nodal bases: the tensor-product kernel (sipg_cart.cuh); the Hermite-like
-  // basis keeps the collocation CART kernels
-  tensor_ = cart_ && basis_ != 2 && !std::getenv("DGX_NO_TENSOR");
+  // the tensor-product kernel (sipg_cart.cuh) instead of the collocation
+  // CART kernels
+  tensor_ = cart_ && !std::getenv("DGX_NO_TENSOR");
   if (precision_ == 1)
     {
       cell_geo_f_.resize(cell_geo_.size());

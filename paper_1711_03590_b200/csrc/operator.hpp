@@ -113,7 +113,7 @@ private:
   RankLayout layout_;
   bool compressed_ = false;
   bool cart_ = false; // compressed records axis-aligned (CART kernels)
-  bool tensor_ = false; // ... and a nodal basis: the tensor-product kernel (sipg_cart.cuh)
+  bool tensor_ = false; // ... run the tensor-product kernel (sipg_cart.cuh)
   bool host_only_ = false;
   std::vector<int> host_task_slot_, host_task_geo_;
   std::vector<int2> host_task_face_;

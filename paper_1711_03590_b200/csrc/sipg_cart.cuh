@@ -20,13 +20,32 @@
 // reference (the k-point Gauss rule is inside M1 and K1), so the results agree
 // to round-off; the sum order differs like in the collocation kernels.
 //
-// Thread layout as sipg_apply_kernel: P = K^{D-1} threads per cell, thread p
-// holds one nodal line along the current axis in registers; 1D matrices are
-// mirror-symmetric and applied in even-odd form from the constant bank.
+// P = K^{D-1} threads per cell; a thread holds one nodal line along the
+// current axis in registers; the 1D matrices are mirror-symmetric and applied
+// in even-odd form from the constant bank.
 //   3D:  z: t_z -> C;  x: t_x -> A, C <- M_x C;  y: t_y -> B, A <- M_y A,
 //        C <- M_y C;  x: A <- A + M_x B;  z: y = M_z A + C.
 // 17 shared-memory field passes and 9 1D products per cell, against 59 and 12
 // (+ the face phase) of the collocation kernels.
+//
+// The kernel is bound by the L1 / shared-memory data pipe (ncu: 91% busy in
+// its first version), so the layout is built around wavefronts:
+// * every global access is coalesced: the own cell and all 2D neighbour cells
+//   are read as flat runs (thread t reads elements t + P m); the cells across
+//   the x- and y-faces are staged in shared memory and the thread then reads
+//   its neighbour lines from there (a thread-contiguous x-line read from HBM
+//   costs one sector per lane and request);
+// * volume fields have row stride K and a plane stride S2 = K^2 + pad chosen
+//   per K and word size so that the bank residues of the lines along x and
+//   along y are (nearly) evenly spread; a per-axis permutation of the lines
+//   over the threads (host-built, constant memory) then makes the residue of
+//   thread t equal t + beta mod #banks, and a cell stride = P mod #banks
+//   continues that run across the cells of a CTA: consecutive lanes hit
+//   consecutive banks for every axis, whatever the warp alignment.
+// * each neighbour line is reduced at once to the two scalars a face needs.
+// Hermite-like basis: the sign-flipped tables (mirror-symmetric M1, K1), the
+// sign applied to u and y, two values per neighbour line read directly (only
+// they are shipped for a ghost cell), masked ghost cells.
 #pragma once
 
 namespace dgx
@@ -34,25 +53,77 @@ namespace dgx
 namespace dev
 {
 
+// plane-stride padding (3D) per K = 2..11 for 8-byte and 4-byte words (16 / 32
+// banks): offline search for evenly spread line residues, pad <= 8
+constexpr int cart_pad(int K, int wbytes)
+{
+  constexpr int p8[10] = {0, 5, 3, 5, 3, 1, 7, 1, 3, 4};
+  constexpr int p4[10] = {0, 5, 3, 3, 1, 3, 7, 3, 3, 0};
+  return (K < 2 || K > 11) ? 0 : (wbytes == 8 ? p8[K - 2] : p4[K - 2]);
+}
+
 template <typename Real, int D, int K>
 struct CartShape
 {
-  using L = SL<D, K>;
-  static constexpr int P = L::P;
-  static constexpr int FS = L::FS;
-  static constexpr int NF = D == 3 ? 4 : 3; // U, A, B (, C)
-  static constexpr int SM_CELL = NF * FS;
+  static constexpr int P = ipow_c(K, D - 1);
+  static constexpr int NBANK = 128 / (int)sizeof(Real); // banks of one word
+  // 3D: rows dense (x + K y = the thread index of a z-line), padded planes;
+  // 2D: odd row stride
+  static constexpr int S1 = D == 3 ? K : K + ((K % 2 == 0) ? 1 : 0);
+  static constexpr int S2 = D == 3 ? K * K + cart_pad(K, (int)sizeof(Real)) : 0;
+  static constexpr int FS = D == 3 ? S2 * K : S1 * K;
+  // U, A, B, C (+ two more neighbour staging fields in 3D)
+  static constexpr int NF = D == 3 ? 6 : 4;
+  // per-cell constants behind the fields: per face (JxW_f, jo, jb, tau), per
+  // axis the cell coefficient, then 2D x (neighbour slot, own side) as ints
+  static constexpr int OFF_FC = NF * FS;
+  static constexpr int OFF_CC = OFF_FC + 8 * D;
+  static constexpr int OFF_TF = OFF_CC + D;
+  static constexpr int SM_MIN = OFF_TF + 4 * D;
+  // cell stride = P mod #banks (3D): the bank run continues across cells
+  static constexpr int SM_CELL = D == 3 ? SM_MIN + ((P % NBANK) - (SM_MIN % NBANK) + NBANK) % NBANK
+                                        : (SM_MIN + 1) / 2 * 2;
   static constexpr int NC = (192 / P) > 0 ? 192 / P : 1;
   static constexpr int THREADS = NC * P;
   static constexpr int SMEM_REALS = NC * SM_CELL;
-  // registers: four lines of K values (own, result, two neighbours)
-  static constexpr int REGS = 4 * K * (int)(sizeof(Real) / 4) + 40;
+  // registers: two lines of K values and the neighbour scalars (measured at
+  // k = 7, C5: 4 CTAs per SM 19.8 ms, 3 CTAs 23.6 ms, 5 CTAs (spills) 21.9 ms)
+  static constexpr int REGS = (2 * K + 4 * D) * (int)(sizeof(Real) / 4) + 40;
   static constexpr int WARP_THREADS = (THREADS + 31) / 32 * 32;
-  static constexpr int MB_REGS = 65536 / (WARP_THREADS * REGS);
+  static constexpr int MB_REGS = 65536 / (WARP_THREADS * REGS) - (K >= 9 && sizeof(Real) == 8 ? 1 : 0);
   static constexpr int MB_SMEM = (220 * 1024) / (SMEM_REALS * (int)sizeof(Real) + 1024);
   static constexpr int MB0 = MB_REGS < MB_SMEM ? MB_REGS : MB_SMEM;
+#ifdef DGX_CART_MINB
+  static constexpr int MINB = DGX_CART_MINB;
+#else
   static constexpr int MINB = MB0 < 1 ? 1 : (MB0 > 6 ? 6 : MB0);
+#endif
 };
+
+// line permutations of the 3D kernel, [fp64 / fp32][K][axis 0 / 1][thread]
+static __constant__ unsigned char c_cart_perm[2][kMaxK + 1][2][128];
+
+// shared-memory offset of entry m of line l along axis A
+template <typename Real, int D, int K, int A>
+__device__ __forceinline__ int cidx(int l, int m)
+{
+  using CS = CartShape<Real, D, K>;
+  return lidx<D, K, A, CS::S1, CS::S2>(l, m);
+}
+template <typename Real, int D, int K, int A>
+__device__ __forceinline__ void cload(const Real *f, int l, Real (&x)[K])
+{
+#pragma unroll
+  for (int m = 0; m < K; ++m)
+    x[m] = f[cidx<Real, D, K, A>(l, m)];
+}
+template <typename Real, int D, int K, int A>
+__device__ __forceinline__ void cstore(Real *f, int l, const Real (&x)[K])
+{
+#pragma unroll
+  for (int m = 0; m < K; ++m)
+    f[cidx<Real, D, K, A>(l, m)] = x[m];
+}
 
 template <typename Real, int K>
 __device__ __forceinline__ void apply_M1(const Real (&x)[K], Real (&y)[K])
@@ -60,22 +131,82 @@ __device__ __forceinline__ void apply_M1(const Real (&x)[K], Real (&y)[K])
   eo_sym<Real, K, TabLayout<K>::oM1E, TabLayout<K>::oM1O>(x, y);
 }
 
-// One face (side S of the line's axis A) of the line operator: adds
-// rv Sf_S^T + g jo Df_S^T to t. u: own nodal line, xn: the neighbour's line
-// through the same face point (zeros if there is none).
-template <typename Real, int D, int K, int A, int S, bool GLN>
-__device__ __forceinline__ void cart_face(const ApplyParams<Real> &prm, const int2 tf,
-                                          const Real (&u)[K], const Real (&xn)[K], Real (&t)[K])
+// The neighbour's face value and normal derivative on the nodal line p along
+// axis A, for both faces of the axis: everything a face needs from the cell
+// across it. Issued for all axes at task start (every global load of the
+// task is in flight at once).
+template <typename Real, int D, int K, int A, bool GLN, bool HERM>
+__device__ __forceinline__ void cart_nb(const ApplyParams<Real> &prm, const int2 (&tf)[2 * D], int p, Real sp,
+                                        Real (&nu)[2], Real (&nd)[2])
 {
   using T = TabLayout<K>;
+  constexpr int NQ = ipow_c(K, D);
+  if constexpr (HERM)
+    {
+      // Hermite-like: only the two layers next to the face carry a value or a
+      // normal derivative there (read_face_dofs, dof_layout.hpp:291-336) --
+      // and only they are shipped for a ghost neighbour
+#pragma unroll
+      for (int s = 0; s < 2; ++s)
+        {
+          const int nbs = tf[2 * A + s].x;
+          const Real *un = prm.u + (long long)(nbs >= 0 ? nbs : 0) * NQ;
+          const int me = s == 0 ? K - 1 : 0, mi = s == 0 ? K - 2 : 1, ro = s == 0 ? K : 0;
+          Real ve = nbs >= 0 ? __ldg(un + gidx<D, K, A>(p, me)) : Real(0);
+          Real vi = nbs >= 0 ? __ldg(un + gidx<D, K, A>(p, mi)) : Real(0);
+          ve *= sp * hsign<Real, K>(me);
+          vi *= sp * hsign<Real, K>(mi);
+          nu[s] = tab<Real, K>(T::oSf + ro + me) * ve + tab<Real, K>(T::oSf + ro + mi) * vi;
+          nd[s] = tab<Real, K>(T::oDf + ro + me) * ve + tab<Real, K>(T::oDf + ro + mi) * vi;
+        }
+      return;
+    }
+  Real xn[2][K];
+#pragma unroll
+  for (int s = 0; s < 2; ++s)
+    {
+      const int nbs = tf[2 * A + s].x;
+      const Real *un = prm.u + (long long)(nbs >= 0 ? nbs : 0) * NQ;
+#pragma unroll
+      for (int m = 0; m < K; ++m)
+        xn[s][m] = nbs >= 0 ? __ldg(un + gidx<D, K, A>(p, m)) : Real(0);
+    }
+  // face s = 0 (low side): the neighbour's high end, and vice versa
+  nu[0] = GLN ? xn[0][K - 1] : dot_row<Real, K, T::oSf + K>(xn[0]);
+  nd[0] = dot_row<Real, K, T::oDf + K>(xn[0]);
+  nu[1] = GLN ? xn[1][0] : dot_row<Real, K, T::oSf>(xn[1]);
+  nd[1] = dot_row<Real, K, T::oDf>(xn[1]);
+}
+
+// The same two scalars from neighbour cells staged in shared memory (fields
+// F0: across the low face, F1: across the high face; line l along A)
+template <typename Real, int D, int K, int A, bool GLN>
+__device__ __forceinline__ void cart_nb_staged(const Real *F0, const Real *F1, int l, Real (&nu)[2], Real (&nd)[2])
+{
+  using T = TabLayout<K>;
+  Real xn[K];
+  cload<Real, D, K, A>(F0, l, xn);
+  nu[0] = GLN ? xn[K - 1] : dot_row<Real, K, T::oSf + K>(xn);
+  nd[0] = dot_row<Real, K, T::oDf + K>(xn);
+  cload<Real, D, K, A>(F1, l, xn);
+  nu[1] = GLN ? xn[0] : dot_row<Real, K, T::oSf>(xn);
+  nd[1] = dot_row<Real, K, T::oDf>(xn);
+}
+
+// One face (side S of the line's axis A) of the line operator: adds
+// rv Sf_S^T + g jo Df_S^T to t. u: own nodal line; nu, nd: the neighbour's
+// face value and normal derivative (reference coordinates) on the same line.
+template <typename Real, int D, int K, int A, int S, bool GLN>
+__device__ __forceinline__ void cart_face(const Real *cell, const Real (&u)[K], Real nu, Real nd, Real (&t)[K])
+{
+  using T = TabLayout<K>;
+  using CS = CartShape<Real, D, K>;
+  const int *tfs = reinterpret_cast<const int *>(cell + CS::OFF_TF);
+  const int2 tf = make_int2(tfs[2 * (2 * A + S)], tfs[2 * (2 * A + S) + 1]);
   if (tf.x == -2)
     return; // not computed on this rank (arrives by compress)
-  const int fid = tf.y & 0x3fffffff;
-  const int side = (tf.y >> 30) & 1;
-  const Real *fg = prm.face_geo + (long long)fid * (2 * D + 1);
-  const Real jx = __ldg(fg);
-  const Real jo = __ldg(fg + 1 + side * D + A);
-  const Real tau = __ldg(prm.penalty + fid);
+  const Real *fc = cell + CS::OFF_FC + 4 * (2 * A + S);
+  const Real jx = fc[0], jo = fc[1], tau = fc[3];
   const Real uf = GLN ? (S == 0 ? u[0] : u[K - 1]) : dot_row<Real, K, T::oSf + S * K>(u);
   const Real dno = dot_row<Real, K, T::oDf + S * K>(u) * jo;
   Real rv, g;
@@ -87,10 +218,8 @@ __device__ __forceinline__ void cart_face(const ApplyParams<Real> &prm, const in
     }
   else
     {
-      const Real jb = __ldg(fg + 1 + (1 - side) * D + A);
-      const Real nu = GLN ? (S == 0 ? xn[K - 1] : xn[0]) : dot_row<Real, K, T::oSf + (1 - S) * K>(xn);
-      const Real dnb = dot_row<Real, K, T::oDf + (1 - S) * K>(xn) * jb;
-      const Real sgn = side == 0 ? Real(1) : Real(-1);
+      const Real dnb = nd * fc[2];
+      const Real sgn = tf.y == 0 ? Real(1) : Real(-1);
       const Real delta = uf - nu;
       rv = (delta * tau - sgn * ((dno + dnb) * Real(0.5))) * jx;
       g = -(sgn * delta * jx * Real(0.5));
@@ -112,49 +241,35 @@ __device__ __forceinline__ void cart_face(const ApplyParams<Real> &prm, const in
     }
 }
 
-// t = L_A u for the nodal line p along axis A of the task's cell
+// t = L_A u for one nodal line along axis A of the task's cell
 template <typename Real, int D, int K, int A, bool GLN>
-__device__ __forceinline__ void cart_line(const ApplyParams<Real> &prm, bool active, const int2 *tfp,
-                                          int geo, int p, const Real (&u)[K], Real (&t)[K])
+__device__ __forceinline__ void cart_line(const Real *cell, const Real (&u)[K], const Real (&nu)[2],
+                                          const Real (&nd)[2], Real (&t)[K])
 {
   using T = TabLayout<K>;
-  constexpr int NQ = ipow_c(K, D);
-  int2 tf[2];
-  Real xn[2][K];
-#pragma unroll
-  for (int s = 0; s < 2; ++s)
-    {
-      tf[s] = active ? __ldg(tfp + 2 * A + s) : make_int2(-2, 0);
-      const bool nb = tf[s].x >= 0;
-      const Real *un = prm.u + (long long)(nb ? tf[s].x : 0) * NQ;
-#pragma unroll
-      for (int m = 0; m < K; ++m)
-        xn[s][m] = nb ? __ldg(un + gidx<D, K, A>(p, m)) : Real(0);
-    }
-  Real c = Real(0);
-  if (geo >= 0)
-    {
-      const Real *cg = prm.cell_geo + (long long)geo * (D * D + 1);
-      const Real j = __ldg(cg + A * D + A);
-      c = (j * j) * __ldg(cg + D * D);
-    }
+  const Real c = cell[CartShape<Real, D, K>::OFF_CC + A];
   eo_sym<Real, K, T::oK1E, T::oK1O>(u, t);
 #pragma unroll
   for (int m = 0; m < K; ++m)
     t[m] *= c;
-  cart_face<Real, D, K, A, 0, GLN>(prm, tf[0], u, xn[0], t);
-  cart_face<Real, D, K, A, 1, GLN>(prm, tf[1], u, xn[1], t);
+  cart_face<Real, D, K, A, 0, GLN>(cell, u, nu[0], nd[0], t);
+  cart_face<Real, D, K, A, 1, GLN>(cell, u, nu[1], nd[1], t);
 }
 
 template <typename Real, int D, int K, int BASIS>
 __global__ void __launch_bounds__(CartShape<Real, D, K>::THREADS, CartShape<Real, D, K>::MINB)
   sipg_cart_kernel(const ApplyParams<Real> prm)
 {
-  static_assert(BASIS != 2, "the Hermite-like basis runs the collocation kernels");
   using CS = CartShape<Real, D, K>;
-  using L = SL<D, K>;
-  constexpr int P = L::P, NQ = L::NQ, FS = L::FS, NC = CS::NC;
-  constexpr bool GLN = BASIS == 0;
+  constexpr int P = CS::P, NQ = P * K, FS = CS::FS, NC = CS::NC;
+  constexpr bool GLN = BASIS == 0, HERM = BASIS == 2;
+  // neighbour cells across the x- / y-faces staged in shared memory: pays in
+  // fp64, where the L1 data pipe binds (C5: 19.8 -> 19.3 ms); fp32 and the
+  // two-value Hermite-like reads go to HBM / L2 directly (C5 fp32: 11.2 vs 11.6 ms)
+#ifndef DGX_CART_STAGE
+#define DGX_CART_STAGE 8
+#endif
+  constexpr bool STAGE = !HERM && (int)sizeof(Real) >= DGX_CART_STAGE;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   Real *smem = reinterpret_cast<Real *>(smem_raw);
   const int lc = threadIdx.x / P;
@@ -162,77 +277,184 @@ __global__ void __launch_bounds__(CartShape<Real, D, K>::THREADS, CartShape<Real
   const int task = blockIdx.x * NC + lc;
   const bool active = task < prm.n_tasks;
   Real *U = smem + lc * CS::SM_CELL;
-  Real *Af = U + FS;
-  Real *Bf = Af + FS;
+  Real *Af = U + FS;      // staging: cell across the low x-face; then t_x, ...
+  Real *Bf = Af + FS;     // staging: cell across the high x-face; then t_y
+  Real *Cf = Bf + FS;     // t of the last axis
   const int slot = active ? prm.task_slot[task] : 0;
   const int geo = active ? prm.task_geo[task] : -1;
   const int2 *tfp = prm.task_face + (long long)(active ? task : 0) * 2 * D;
 
+  // the lines this thread owns in the x- and y-phases (bank-spreading
+  // permutations, 3D), and in the last-axis phases: line p
+  int p0 = p, p1 = p;
+  if constexpr (D == 3)
+    {
+      p0 = c_cart_perm[sizeof(Real) == 8 ? 0 : 1][K][0][p];
+      p1 = c_cart_perm[sizeof(Real) == 8 ? 0 : 1][K][1][p];
+    }
+
+  // ---- every global load of the task: face entries, own cell, neighbour
+  //      cells (coalesced; reduced to two scalars per line), constants -------
+  int2 tf[2 * D];
+#pragma unroll
+  for (int phi = 0; phi < 2 * D; ++phi)
+    tf[phi] = active ? __ldg(tfp + phi) : make_int2(-2, 0);
+  // Hermite-like basis (tables of the sign-flipped functions, setup.hpp
+  // Tables1D): sign of a line's two tangential indices -- the digits of its
+  // line number -- and, for a ghost-side task, the layers that were shipped
+  Real sp = Real(1), sp0 = Real(1), sp1 = Real(1);
+  unsigned gmask = (1u << K) - 1u;
+  if constexpr (HERM)
+    {
+      sp = hsign<Real, K>(p % K);
+      sp0 = hsign<Real, K>(p0 % K);
+      sp1 = hsign<Real, K>(p1 % K);
+      if constexpr (D == 3)
+        {
+          sp *= hsign<Real, K>(p / K);
+          sp0 *= hsign<Real, K>(p0 / K);
+          sp1 *= hsign<Real, K>(p1 / K);
+        }
+      if (active && slot >= prm.n_owned)
+        gmask = ghost_layer_mask<D, K, 2>(tf, p);
+    }
   Real x[K], t[K];
-  // last axis: the thread's line is contiguous across threads in HBM
   {
+    // last axis: the thread's line is contiguous across threads in HBM
     const Real *uc = prm.u + (long long)slot * NQ;
 #pragma unroll
     for (int m = 0; m < K; ++m)
-      x[m] = active ? __ldg(uc + p + P * m) : Real(0);
+      {
+        x[m] = active ? __ldg(uc + p + P * m) : Real(0);
+        if constexpr (HERM)
+          x[m] = ((gmask >> m) & 1u) ? x[m] * (sp * hsign<Real, K>(m)) : Real(0);
+      }
   }
-  cart_line<Real, D, K, D - 1, GLN>(prm, active, tfp, geo, p, x, t);
-  store_pencil<Real, D, K, D - 1>(U, p, x);
-  if constexpr (D == 3)
+  Real nu[D][2], nd[D][2];
+  cart_nb<Real, D, K, D - 1, GLN, HERM>(prm, tf, p, sp, nu[D - 1], nd[D - 1]);
+  if constexpr (!STAGE)
     {
-      Real *Cf = Bf + FS;
-      store_pencil<Real, D, K, 2>(Cf, p, t); // t_z
-      __syncthreads();
-      load_pencil<Real, D, K, 0>(U, p, x);
-      cart_line<Real, D, K, 0, GLN>(prm, active, tfp, geo, p, x, t);
-      store_pencil<Real, D, K, 0>(Af, p, t); // t_x
-      load_pencil<Real, D, K, 0>(Cf, p, x);
-      apply_M1<Real, K>(x, t);
-      store_pencil<Real, D, K, 0>(Cf, p, t); // M_x t_z
-      __syncthreads();
-      load_pencil<Real, D, K, 1>(U, p, x);
-      cart_line<Real, D, K, 1, GLN>(prm, active, tfp, geo, p, x, t);
-      store_pencil<Real, D, K, 1>(Bf, p, t); // t_y
-      load_pencil<Real, D, K, 1>(Af, p, x);
-      apply_M1<Real, K>(x, t);
-      store_pencil<Real, D, K, 1>(Af, p, t); // M_y t_x
-      load_pencil<Real, D, K, 1>(Cf, p, x);
-      apply_M1<Real, K>(x, t);
-      store_pencil<Real, D, K, 1>(Cf, p, t); // M_y M_x t_z
-      __syncthreads();
-      load_pencil<Real, D, K, 0>(Bf, p, x);
-      apply_M1<Real, K>(x, t);
-      load_pencil<Real, D, K, 0>(Af, p, x);
-#pragma unroll
-      for (int m = 0; m < K; ++m)
-        t[m] += x[m];
-      store_pencil<Real, D, K, 0>(Af, p, t); // M_y t_x + M_x t_y
-      __syncthreads();
-      load_pencil<Real, D, K, 2>(Af, p, x);
-      apply_M1<Real, K>(x, t);
-      load_pencil<Real, D, K, 2>(Cf, p, x);
+      cart_nb<Real, D, K, 0, GLN, HERM>(prm, tf, p0, sp0, nu[0], nd[0]);
+      if constexpr (D == 3)
+        cart_nb<Real, D, K, 1, GLN, HERM>(prm, tf, p1, sp1, nu[1], nd[1]);
     }
   else
     {
-      store_pencil<Real, D, K, 1>(Af, p, t); // t_y
-      __syncthreads();
-      load_pencil<Real, D, K, 0>(U, p, x);
-      cart_line<Real, D, K, 0, GLN>(prm, active, tfp, geo, p, x, t);
-      store_pencil<Real, D, K, 0>(Bf, p, t); // t_x
-      load_pencil<Real, D, K, 0>(Af, p, x);
+      // the cells across the x- (and y-) faces, staged like U
+#pragma unroll
+      for (int phi = 0; phi < 2 * (D - 1); ++phi)
+        {
+          Real *F = phi < 2 ? Af + phi * FS : Cf + (phi - 1) * FS; // 3D: fields 4, 5 behind C
+          const int nbs = tf[phi].x;
+          const Real *un = prm.u + (long long)(nbs >= 0 ? nbs : 0) * NQ;
+          Real v[K];
+#pragma unroll
+          for (int m = 0; m < K; ++m)
+            v[m] = nbs >= 0 ? __ldg(un + p + P * m) : Real(0);
+          cstore<Real, D, K, D - 1>(F, p, v);
+        }
+    }
+  cstore<Real, D, K, D - 1>(U, p, x);
+  for (int phi = p; phi < 2 * D; phi += P)
+    {
+      int2 f = make_int2(-2, 0);
+#pragma unroll
+      for (int i = 0; i < 2 * D; ++i)
+        f = (i == phi) ? tf[i] : f;
+      Real *fc = U + CS::OFF_FC + 4 * phi;
+      int side = 0;
+      if (f.x != -2)
+        {
+          const int fid = f.y & 0x3fffffff;
+          side = (f.y >> 30) & 1;
+          const int a = phi / 2;
+          const Real *fg = prm.face_geo + (long long)fid * (2 * D + 1);
+          fc[0] = __ldg(fg);
+          fc[1] = __ldg(fg + 1 + side * D + a);
+          fc[2] = __ldg(fg + 1 + (1 - side) * D + a);
+          fc[3] = __ldg(prm.penalty + fid);
+        }
+      int *tfs = reinterpret_cast<int *>(U + CS::OFF_TF);
+      tfs[2 * phi] = f.x;
+      tfs[2 * phi + 1] = side;
+    }
+  for (int a = p; a < D; a += P)
+    {
+      Real c = Real(0);
+      if (geo >= 0)
+        {
+          // (J^{-T}_aa)^2 det J; off-diagonal round-off (<= 1e-13 relative) dropped
+          const Real *cg = prm.cell_geo + (long long)geo * (D * D + 1);
+          const Real j = __ldg(cg + a * D + a);
+          c = (j * j) * __ldg(cg + D * D);
+        }
+      U[CS::OFF_CC + a] = c;
+    }
+  __syncthreads();
+
+  // last axis (line p, in registers since the load)
+  cart_line<Real, D, K, D - 1, GLN>(U, x, nu[D - 1], nd[D - 1], t);
+  cstore<Real, D, K, D - 1>(Cf, p, t);
+  if constexpr (STAGE)
+    {
+      cart_nb_staged<Real, D, K, 0, GLN>(Af, Bf, p0, nu[0], nd[0]);
+      if constexpr (D == 3)
+        cart_nb_staged<Real, D, K, 1, GLN>(Cf + FS, Cf + 2 * FS, p1, nu[1], nd[1]);
+    }
+  cload<Real, D, K, 0>(U, p0, x);
+  cart_line<Real, D, K, 0, GLN>(U, x, nu[0], nd[0], t); // t_x, kept in registers
+  __syncthreads(); // staging fields free, C complete
+  if constexpr (D == 3)
+    {
+      cstore<Real, D, K, 0>(Af, p0, t); // t_x
+      cload<Real, D, K, 0>(Cf, p0, x);
       apply_M1<Real, K>(x, t);
-      store_pencil<Real, D, K, 0>(Af, p, t); // M_x t_y
+      cstore<Real, D, K, 0>(Cf, p0, t); // M_x t_z
       __syncthreads();
-      load_pencil<Real, D, K, 1>(Bf, p, x);
+      cload<Real, D, K, 1>(U, p1, x);
+      cart_line<Real, D, K, 1, GLN>(U, x, nu[1], nd[1], t);
+      cstore<Real, D, K, 1>(Bf, p1, t); // t_y
+      cload<Real, D, K, 1>(Af, p1, x);
       apply_M1<Real, K>(x, t);
-      load_pencil<Real, D, K, 1>(Af, p, x);
+      cstore<Real, D, K, 1>(Af, p1, t); // M_y t_x
+      cload<Real, D, K, 1>(Cf, p1, x);
+      apply_M1<Real, K>(x, t);
+      cstore<Real, D, K, 1>(Cf, p1, t); // M_y M_x t_z
+      __syncthreads();
+      cload<Real, D, K, 0>(Bf, p0, x);
+      apply_M1<Real, K>(x, t);
+      cload<Real, D, K, 0>(Af, p0, x);
+#pragma unroll
+      for (int m = 0; m < K; ++m)
+        t[m] += x[m];
+      cstore<Real, D, K, 0>(Af, p0, t); // M_y t_x + M_x t_y
+      __syncthreads();
+      cload<Real, D, K, 2>(Af, p, x);
+      apply_M1<Real, K>(x, t);
+      cload<Real, D, K, 2>(Cf, p, x);
+    }
+  else
+    {
+      cstore<Real, D, K, 0>(Bf, p0, t); // t_x
+      cload<Real, D, K, 0>(Cf, p0, x);
+      apply_M1<Real, K>(x, t);
+      cstore<Real, D, K, 0>(Cf, p0, t); // M_x t_y
+      __syncthreads();
+      cload<Real, D, K, 1>(Bf, p, x);
+      apply_M1<Real, K>(x, t);
+      cload<Real, D, K, 1>(Cf, p, x);
     }
   if (active)
     {
       Real *yc = prm.y + (long long)slot * NQ;
 #pragma unroll
       for (int m = 0; m < K; ++m)
-        __stcs(yc + p + P * m, t[m] + x[m]); // y is not read again (streaming)
+        {
+          Real v = t[m] + x[m];
+          if constexpr (HERM)
+            v = ((gmask >> m) & 1u) ? v * (sp * hsign<Real, K>(m)) : Real(0);
+          __stcs(yc + p + P * m, v); // y is not read again (streaming)
+        }
     }
 }
 

@@ -12,7 +12,9 @@
 #include "sipg_rhs.cuh"
 #include "sipg_adv.cuh"
 
+#include <algorithm>
 #include <mutex>
+#include <vector>
 #include <set>
 #include <tuple>
 
@@ -162,7 +164,6 @@ void launch_pairs(const dev::ApplyParams<double> &prm, cudaStream_t s)
 template <typename Real, int D, int K>
 void launch_cart(const dev::ApplyParams<Real> &prm, cudaStream_t s)
 {
-#if DGX_BASIS != 2
   using CS = dev::CartShape<Real, D, K>;
   const size_t smem = (size_t)CS::SMEM_REALS * sizeof(Real);
   auto kern = dev::sipg_cart_kernel<Real, D, K, DGX_BASIS>;
@@ -172,10 +173,6 @@ void launch_cart(const dev::ApplyParams<Real> &prm, cudaStream_t s)
   if (grid > 0)
     kern<<<grid, CS::THREADS, smem, s>>>(prm);
   cuda_check(cudaGetLastError(), "sipg_cart_kernel launch");
-#else
-  (void)prm, (void)s;
-  fail(Code::logic_error, "sipg_cart_kernel: not built for the Hermite-like basis");
-#endif
 }
 
 #ifndef DGX_CART_PAIRS
@@ -185,7 +182,7 @@ void launch_cart(const dev::ApplyParams<Real> &prm, cudaStream_t s)
 template <typename Real, int D, int K, bool C, bool CART = false>
 void launch_one(const dev::ApplyParams<Real> &prm, cudaStream_t s)
 {
-  if constexpr (C && !CART && DGX_BASIS != 2)
+  if constexpr (C && !CART)
     if (prm.cart == 2)
       {
         launch_cart<Real, D, K>(prm, s);
@@ -405,6 +402,77 @@ void DGX_FN(launch_adv)(int D, int K, bool compressed, const dev::AdvParams<doub
 #endif
 }
 
+// Line permutations of the tensor-product kernel (sipg_cart.cuh): thread t of
+// a cell owns, in the x- and y-phases, a line whose first entry lies in bank
+// (t + beta) mod #banks -- lines are handed out greedily by bank residue, the
+// few that do not fit the run fill the gaps.
+template <typename Real, int K>
+void cart_perm_host(unsigned char (&out)[2][128])
+{
+  using CS = dev::CartShape<Real, 3, K>;
+  constexpr int P = K * K, NB = CS::NBANK;
+  for (int A = 0; A < 2; ++A)
+    {
+      std::vector<int> res(P);
+      for (int l = 0; l < P; ++l)
+        {
+          const int i = l % K, j = l / K;
+          res[l] = (A == 0 ? CS::S1 * i + CS::S2 * j : i + CS::S2 * j) % NB;
+        }
+      int best_bad = 1 << 30, beta = 0;
+      for (int b = 0; b < NB; ++b)
+        {
+          std::vector<int> need(NB, 0), have(NB, 0);
+          for (int t = 0; t < P; ++t)
+            {
+              ++need[(t + b) % NB];
+              ++have[res[t]];
+            }
+          int bad = 0;
+          for (int r = 0; r < NB; ++r)
+            bad += std::max(0, need[r] - have[r]);
+          if (bad < best_bad)
+            {
+              best_bad = bad;
+              beta = b;
+            }
+        }
+      std::vector<int> line_of(P, -1);
+      std::vector<char> used(P, 0);
+      for (int t = 0; t < P; ++t)
+        for (int l = 0; l < P; ++l)
+          if (!used[l] && res[l] == (t + beta) % NB)
+            {
+              line_of[t] = l;
+              used[l] = 1;
+              break;
+            }
+      int next = 0;
+      for (int t = 0; t < P; ++t)
+        if (line_of[t] < 0)
+          {
+            while (used[next])
+              ++next;
+            line_of[t] = next;
+            used[next] = 1;
+          }
+      for (int t = 0; t < 128; ++t)
+        out[A][t] = static_cast<unsigned char>(t < P ? line_of[t] : 0);
+    }
+}
+
+template <int K>
+void upload_cart_perm()
+{
+  unsigned char h[2][128];
+  cart_perm_host<double, K>(h);
+  cuda_check(cudaMemcpyToSymbol(dev::c_cart_perm, h, sizeof h, (size_t)(0 * (dev::kMaxK + 1) + K) * sizeof h),
+             "upload line permutations");
+  cart_perm_host<float, K>(h);
+  cuda_check(cudaMemcpyToSymbol(dev::c_cart_perm, h, sizeof h, (size_t)(1 * (dev::kMaxK + 1) + K) * sizeof h),
+             "upload line permutations");
+}
+
 void DGX_FN(upload_tables)(int K)
 {
   int devid = 0;
@@ -420,6 +488,15 @@ void DGX_FN(upload_tables)(int K)
   cuda_check(cudaMemcpyToSymbol(dev::c_tab_f, tf.data(), tf.size() * sizeof(float),
                                 dev::tab_offset(K) * sizeof(float)),
              "upload tables");
+  switch (K)
+    {
+#define DGX_PERM_K(KK)                                                                     \
+  case KK: upload_cart_perm<KK>(); break;
+      DGX_PERM_K(2) DGX_PERM_K(3) DGX_PERM_K(4) DGX_PERM_K(5) DGX_PERM_K(6) DGX_PERM_K(7)
+      DGX_PERM_K(8) DGX_PERM_K(9) DGX_PERM_K(10) DGX_PERM_K(11)
+#undef DGX_PERM_K
+    default: break;
+    }
   g_uploaded.insert({devid, K});
 }
 

@@ -285,8 +285,8 @@ def test_ny_beyond_one_tile(torch):
 ])
 @pytest.mark.parametrize("precision", ["fp64", "fp32"])
 def test_cart_kernel(torch, d, cells, p, periodic, basis, precision):
-    """Cartesian box meshes run the tensor-product kernel (nodal bases) or the
-    collocation CART kernels (Hermite-like basis, DGX_NO_TENSOR; axis-aligned
+    """Cartesian box meshes run the tensor-product kernel or the
+    collocation CART kernels (DGX_NO_TENSOR; axis-aligned
     affine records: the tangential face terms, products with round-off zeros,
     are skipped): flagged in stats, equal to the general kernel (DGX_NO_CART)
     to round-off and to the C restatement within the parity tolerance."""
@@ -309,9 +309,8 @@ def test_cart_kernel(torch, d, cells, p, periodic, basis, precision):
         col = D.RankOperator(mesh, part, faces, D.Geometry(), cfg)
     finally:
         del os.environ["DGX_NO_TENSOR"]
-    # nodal bases: the tensor-product kernel (2); Hermite-like and DGX_NO_TENSOR: the
-    # collocation CART kernels (1)
-    assert op.stats()["cartesian"] == (1 if basis == "hermite_like" else 2)
+    # the tensor-product kernel (2); DGX_NO_TENSOR: the collocation CART kernels (1)
+    assert op.stats()["cartesian"] == 2
     assert col.stats()["cartesian"] == 1 and gen.stats()["cartesian"] == 0
     x = D.random_vector(int(np.prod(cells)) * (p + 1) ** d, 9)
     dt = torch.float32 if precision == "fp32" else torch.float64

@@ -463,7 +463,7 @@ def test_fp32_random_against_oracle(torch, cfg):
 
 # Cartesian meshes, nodal bases: the tensor-product kernel (sipg_cart.cuh) against the
 # oracle -- every degree in 2D and 3D, Dirichlet and periodic, 1-3 ranks (ghost-side
-# tasks), both nodal bases, anisotropic cells (cells per direction differ on the unit box)
+# tasks), all three bases, anisotropic cells (cells per direction differ on the unit box)
 CART_TENSOR = (
     [(2, [5, 4], p, p % 2 == 0, None, False, 1 + p % 2) for p in range(1, 11)] +
     [(3, [3, 2, 4], p, p % 2 == 1, None, False, 1) for p in range(1, 8)] +
@@ -472,7 +472,10 @@ CART_TENSOR = (
     [(3, [3, 2, 2], 4, False, None, False, 2, "lagrange_gauss"),
      (3, [2, 3, 2], 5, True, None, False, 1, "lagrange_gauss"),
      (2, [4, 3], 6, False, None, False, 2, "lagrange_gauss"),
-     (2, [3, 3], 3, True, None, False, 1, "lagrange_gauss")]
+     (2, [3, 3], 3, True, None, False, 1, "lagrange_gauss")] +
+    # Hermite-like: two neighbour layers, sign-flipped tables, masked ghost cells
+    [(3, [3, 2, 3], p, p % 2 == 0, None, False, 1 + p % 3, "hermite_like") for p in (3, 4, 5, 7, 10)] +
+    [(2, [4, 5], p, p % 2 == 1, None, False, 1 + p % 2, "hermite_like") for p in (3, 6, 9)]
 )
 
 
