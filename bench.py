@@ -420,6 +420,12 @@ def main():
     ev_b.record(stream)
     ev_b.synchronize()
     first_ms = ev_a.elapsed_time(ev_b)
+    if ws > 1:
+        # every rank must enqueue the same number of applies (each one posts
+        # sends / receives to its neighbours): agree on the slowest rank's time
+        fm = torch.tensor([first_ms], dtype=torch.float64, device=f"cuda:{local}")
+        dist.all_reduce(fm, op=dist.ReduceOp.MAX)
+        first_ms = float(fm.item())
     with ClockSampler(local, load=load if first_ms * args.steps < 1000.0 else None) as clk:
         barrier()
         if flush is None:

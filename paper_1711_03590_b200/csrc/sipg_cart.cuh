@@ -330,6 +330,14 @@ __global__ void __launch_bounds__(CartShape<Real, D, K>::THREADS, CartShape<Real
           x[m] = ((gmask >> m) & 1u) ? x[m] * (sp * hsign<Real, K>(m)) : Real(0);
       }
   }
+  // x-neighbours that are the CTA's previous / next task
+  bool xin[2] = {false, false};
+  if constexpr (STAGE)
+    {
+      xin[0] = active && lc > 0 && tf[0].x >= 0 && tf[0].x == __ldg(prm.task_slot + task - 1);
+      xin[1] = active && lc + 1 < NC && task + 1 < prm.n_tasks && tf[1].x >= 0 &&
+               tf[1].x == __ldg(prm.task_slot + task + 1);
+    }
   Real nu[D][2], nd[D][2];
   cart_nb<Real, D, K, D - 1, GLN, HERM>(prm, tf, p, sp, nu[D - 1], nd[D - 1]);
   if constexpr (!STAGE)
@@ -340,17 +348,21 @@ __global__ void __launch_bounds__(CartShape<Real, D, K>::THREADS, CartShape<Real
     }
   else
     {
-      // the cells across the x- (and y-) faces, staged like U
+      // the cells across the x- (and y-) faces, staged like U -- unless the
+      // cell is the task next door in this CTA (consecutive tasks run along
+      // x): its own field U is read instead
 #pragma unroll
       for (int phi = 0; phi < 2 * (D - 1); ++phi)
         {
           Real *F = phi < 2 ? Af + phi * FS : Cf + (phi - 1) * FS; // 3D: fields 4, 5 behind C
           const int nbs = tf[phi].x;
-          const Real *un = prm.u + (long long)(nbs >= 0 ? nbs : 0) * NQ;
+          if (nbs < 0 || (phi < 2 && xin[phi]))
+            continue; // no neighbour (its scalars are not used), or the CTA partner
+          const Real *un = prm.u + (long long)nbs * NQ;
           Real v[K];
 #pragma unroll
           for (int m = 0; m < K; ++m)
-            v[m] = nbs >= 0 ? __ldg(un + p + P * m) : Real(0);
+            v[m] = __ldg(un + p + P * m);
           cstore<Real, D, K, D - 1>(F, p, v);
         }
     }
@@ -397,7 +409,8 @@ __global__ void __launch_bounds__(CartShape<Real, D, K>::THREADS, CartShape<Real
   cstore<Real, D, K, D - 1>(Cf, p, t);
   if constexpr (STAGE)
     {
-      cart_nb_staged<Real, D, K, 0, GLN>(Af, Bf, p0, nu[0], nd[0]);
+      cart_nb_staged<Real, D, K, 0, GLN>(xin[0] ? U - CS::SM_CELL : Af, xin[1] ? U + CS::SM_CELL : Bf, p0,
+                                         nu[0], nd[0]);
       if constexpr (D == 3)
         cart_nb_staged<Real, D, K, 1, GLN>(Cf + FS, Cf + 2 * FS, p1, nu[1], nd[1]);
     }

@@ -230,3 +230,21 @@ def test_loopback_errors(torch):
     ref = O.Problem(3, [2, 2, 4], 3).apply(x)
     (y,), _ = loopback_apply(torch, ops, x, exs=exs)
     assert rel_linf(y, ref) < TOL64
+
+
+def test_nccl_transport_single_rank(torch):
+    """The NCCL transport with a one-rank communicator: libnccl resolves (the
+    library torch loaded), ncclCommInitRank, grouped calls with no peers; an
+    apply with the exchanger's hooks equals the plain apply. (More ranks need
+    more GPUs: the multi-rank data plane runs over the loopback transport above.)"""
+    D = _dgx()
+    ops = build_ranks(3, [3, 3, 4], 5, 1, geometry=D.Geometry(source="vertex_bump", vertex_bump_eps=0.1))
+    op = ops[0]
+    ex = D.NcclExchanger(op, D.nccl_unique_id())
+    x = D.random_vector(op.layout().total_size, 5)
+    u = torch.tensor(x, device="cuda")
+    y0, y1 = torch.empty_like(u), torch.empty_like(u)
+    op.apply(u, y0)
+    op.apply(u, y1, hooks=ex)
+    torch.cuda.synchronize()
+    assert torch.equal(y0, y1)
