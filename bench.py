@@ -547,6 +547,21 @@ def main():
             cpu = {"value": None, "unit": "DoF/s", "cores": 0, "kind": "reference",
                    "sample": f"unavailable: {ex}"}
 
+    if ws > 1:
+        # tear the communicators down first: with NCCL_DEBUG=INFO their log
+        # lines go to stdout, and the JSON line must be the last one
+        dist.barrier()
+        clk_summary = clk.summary()
+        n_send_plans = len(op.plans("send"))
+        del hooks
+        import gc
+        gc.collect()
+        dist.destroy_process_group()
+        if rank == 0:
+            time.sleep(2.0)  # let the other ranks' teardown lines out first
+    else:
+        clk_summary = clk.summary()
+        n_send_plans = 0
     if rank == 0:
         out = {"metric": metric, "value": value, "unit": "DoF/s", "n_gpus": ws,
                "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
@@ -554,13 +569,10 @@ def main():
                "dtype": "f32" if prec == "fp32" else "f64", "data": "synthetic",
                "config": config, "e2e": e2e,
                "gpu_launches": int(args.steps * st["kernel_launches_per_apply"] +
-                                   (args.steps * (1 + len(op.plans("send"))) if ws > 1 else 0)),
-               "roofline": roofline, "cpu_baseline": cpu, "clocks": clk.summary(),
+                                   (args.steps * (1 + n_send_plans) if ws > 1 else 0)),
+               "roofline": roofline, "cpu_baseline": cpu, "clocks": clk_summary,
                "setup_s": t_setup}
         print(json.dumps(out), flush=True)
-    if ws > 1:
-        dist.barrier()
-        dist.destroy_process_group()
 
 
 if __name__ == "__main__":

@@ -74,12 +74,11 @@ struct CartShape
   static constexpr int FS = D == 3 ? S2 * K : S1 * K;
   // U, A, B, C (+ two more neighbour staging fields in 3D)
   static constexpr int NF = D == 3 ? 6 : 4;
-  // per-cell constants behind the fields: per face (JxW_f, jo, jb, tau), per
-  // axis the cell coefficient, then 2D x (neighbour slot, own side) as ints
+  // per-cell constants behind the fields: three flux coefficients per face
+  // (cart_face), per axis the cell coefficient
   static constexpr int OFF_FC = NF * FS;
-  static constexpr int OFF_CC = OFF_FC + 8 * D;
-  static constexpr int OFF_TF = OFF_CC + D;
-  static constexpr int SM_MIN = OFF_TF + 4 * D;
+  static constexpr int OFF_CC = OFF_FC + 6 * D;
+  static constexpr int SM_MIN = OFF_CC + D;
   // cell stride = P mod #banks (3D): the bank run continues across cells
   static constexpr int SM_CELL = D == 3 ? SM_MIN + ((P % NBANK) - (SM_MIN % NBANK) + NBANK) % NBANK
                                         : (SM_MIN + 1) / 2 * 2;
@@ -179,11 +178,28 @@ __device__ __forceinline__ void cart_nb(const ApplyParams<Real> &prm, const int2
 }
 
 // The same two scalars from neighbour cells staged in shared memory (fields
-// F0: across the low face, F1: across the high face; line l along A)
-template <typename Real, int D, int K, int A, bool GLN>
-__device__ __forceinline__ void cart_nb_staged(const Real *F0, const Real *F1, int l, Real (&nu)[2], Real (&nd)[2])
+// F0: across the low face, F1: across the high face; line l along A, sp: the
+// Hermite-like sign of the line)
+template <typename Real, int D, int K, int A, bool GLN, bool HERM>
+__device__ __forceinline__ void cart_nb_staged(const Real *F0, const Real *F1, int l, Real sp, Real (&nu)[2],
+                                               Real (&nd)[2])
 {
   using T = TabLayout<K>;
+  if constexpr (HERM)
+    {
+      // two layers next to the face (the only ones a ghost cell holds)
+#pragma unroll
+      for (int s = 0; s < 2; ++s)
+        {
+          const Real *F = s == 0 ? F0 : F1;
+          const int me = s == 0 ? K - 1 : 0, mi = s == 0 ? K - 2 : 1, ro = s == 0 ? K : 0;
+          const Real ve = F[cidx<Real, D, K, A>(l, me)] * (sp * hsign<Real, K>(me));
+          const Real vi = F[cidx<Real, D, K, A>(l, mi)] * (sp * hsign<Real, K>(mi));
+          nu[s] = tab<Real, K>(T::oSf + ro + me) * ve + tab<Real, K>(T::oSf + ro + mi) * vi;
+          nd[s] = tab<Real, K>(T::oDf + ro + me) * ve + tab<Real, K>(T::oDf + ro + mi) * vi;
+        }
+      return;
+    }
   Real xn[K];
   cload<Real, D, K, A>(F0, l, xn);
   nu[0] = GLN ? xn[K - 1] : dot_row<Real, K, T::oSf + K>(xn);
@@ -195,36 +211,26 @@ __device__ __forceinline__ void cart_nb_staged(const Real *F0, const Real *F1, i
 
 // One face (side S of the line's axis A) of the line operator: adds
 // rv Sf_S^T + g jo Df_S^T to t. u: own nodal line; nu, nd: the neighbour's
-// face value and normal derivative (reference coordinates) on the same line.
+// face value and normal derivative (reference coordinates) on the same line
+// (zeros without a neighbour). The per-face constants are folded at task
+// start into three coefficients that cover the interior flux
+// (operators.cpp:977-1003), the boundary mirror rule (:1069-1089) and faces not
+// computed on this rank (all zero) without a branch:
+//   rv = A1 (uf - nu) + A2 Df.u + A3 nd,   g jo = A2 (uf - nu)
+//   interior: A1 = tau JxW, A2 = -sgn jo JxW / 2, A3 = -sgn jb JxW / 2
+//   boundary: A1 = 2 tau JxW, A2 = -jo JxW, A3 = 0
 template <typename Real, int D, int K, int A, int S, bool GLN>
 __device__ __forceinline__ void cart_face(const Real *cell, const Real (&u)[K], Real nu, Real nd, Real (&t)[K])
 {
   using T = TabLayout<K>;
   using CS = CartShape<Real, D, K>;
-  const int *tfs = reinterpret_cast<const int *>(cell + CS::OFF_TF);
-  const int2 tf = make_int2(tfs[2 * (2 * A + S)], tfs[2 * (2 * A + S) + 1]);
-  if (tf.x == -2)
-    return; // not computed on this rank (arrives by compress)
-  const Real *fc = cell + CS::OFF_FC + 4 * (2 * A + S);
-  const Real jx = fc[0], jo = fc[1], tau = fc[3];
+  const Real *fc = cell + CS::OFF_FC + 3 * (2 * A + S);
+  const Real a1 = fc[0], a2 = fc[1], a3 = fc[2];
   const Real uf = GLN ? (S == 0 ? u[0] : u[K - 1]) : dot_row<Real, K, T::oSf + S * K>(u);
-  const Real dno = dot_row<Real, K, T::oDf + S * K>(u) * jo;
-  Real rv, g;
-  if (tf.x == -1)
-    {
-      // boundary face, mirror rule (operators.cpp:1069-1089)
-      rv = (uf * tau * Real(2) - dno) * jx;
-      g = -(uf * jx);
-    }
-  else
-    {
-      const Real dnb = nd * fc[2];
-      const Real sgn = tf.y == 0 ? Real(1) : Real(-1);
-      const Real delta = uf - nu;
-      rv = (delta * tau - sgn * ((dno + dnb) * Real(0.5))) * jx;
-      g = -(sgn * delta * jx * Real(0.5));
-    }
-  const Real gj = g * jo;
+  const Real dno = dot_row<Real, K, T::oDf + S * K>(u);
+  const Real delta = uf - nu;
+  const Real rv = a1 * delta + a2 * dno + a3 * nd;
+  const Real gj = a2 * delta;
   if constexpr (GLN)
     {
       // Gauss-Lobatto: Sf rows are exact unit vectors (the end nodes)
@@ -257,19 +263,22 @@ __device__ __forceinline__ void cart_line(const Real *cell, const Real (&u)[K], 
 }
 
 template <typename Real, int D, int K, int BASIS>
-__global__ void __launch_bounds__(CartShape<Real, D, K>::THREADS, CartShape<Real, D, K>::MINB)
+__global__ void __launch_bounds__(CartShape<Real, D, K>::THREADS,
+                                  // Hermite-like: signs, masks and three line numbers more in registers
+                                  (BASIS == 2 && CartShape<Real, D, K>::MINB > 2) ? CartShape<Real, D, K>::MINB - 1
+                                                                                : CartShape<Real, D, K>::MINB)
   sipg_cart_kernel(const ApplyParams<Real> prm)
 {
   using CS = CartShape<Real, D, K>;
   constexpr int P = CS::P, NQ = P * K, FS = CS::FS, NC = CS::NC;
   constexpr bool GLN = BASIS == 0, HERM = BASIS == 2;
-  // neighbour cells across the x- / y-faces staged in shared memory: pays in
-  // fp64, where the L1 data pipe binds (C5: 19.8 -> 19.3 ms); fp32 and the
-  // two-value Hermite-like reads go to HBM / L2 directly (C5 fp32: 11.2 vs 11.6 ms)
+  // neighbour cells across the x- / y-faces staged in shared memory (the L1
+  // data pipe binds in both precisions: C5 fp64 19.8 -> 19.3 ms, fp32 10.8 ->
+  // 10.4 ms); the two-value Hermite-like reads go to HBM / L2 directly
 #ifndef DGX_CART_STAGE
-#define DGX_CART_STAGE 8
+#define DGX_CART_STAGE 4
 #endif
-  constexpr bool STAGE = !HERM && (int)sizeof(Real) >= DGX_CART_STAGE;
+  constexpr bool STAGE = (int)sizeof(Real) >= DGX_CART_STAGE;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   Real *smem = reinterpret_cast<Real *>(smem_raw);
   const int lc = threadIdx.x / P;
@@ -330,9 +339,10 @@ __global__ void __launch_bounds__(CartShape<Real, D, K>::THREADS, CartShape<Real
           x[m] = ((gmask >> m) & 1u) ? x[m] * (sp * hsign<Real, K>(m)) : Real(0);
       }
   }
-  // x-neighbours that are the CTA's previous / next task
+  // x-neighbours that are the CTA's previous / next task (nodal bases: the
+  // Hermite-like U holds sign-flipped, masked values)
   bool xin[2] = {false, false};
-  if constexpr (STAGE)
+  if constexpr (STAGE && !HERM)
     {
       xin[0] = active && lc > 0 && tf[0].x >= 0 && tf[0].x == __ldg(prm.task_slot + task - 1);
       xin[1] = active && lc + 1 < NC && task + 1 < prm.n_tasks && tf[1].x >= 0 &&
@@ -356,13 +366,13 @@ __global__ void __launch_bounds__(CartShape<Real, D, K>::THREADS, CartShape<Real
         {
           Real *F = phi < 2 ? Af + phi * FS : Cf + (phi - 1) * FS; // 3D: fields 4, 5 behind C
           const int nbs = tf[phi].x;
-          if (nbs < 0 || (phi < 2 && xin[phi]))
-            continue; // no neighbour (its scalars are not used), or the CTA partner
-          const Real *un = prm.u + (long long)nbs * NQ;
+          if (phi < 2 && xin[phi])
+            continue; // the CTA partner
+          const Real *un = prm.u + (long long)(nbs >= 0 ? nbs : 0) * NQ;
           Real v[K];
 #pragma unroll
           for (int m = 0; m < K; ++m)
-            v[m] = __ldg(un + p + P * m);
+            v[m] = nbs >= 0 ? __ldg(un + p + P * m) : Real(0); // zeros without a neighbour
           cstore<Real, D, K, D - 1>(F, p, v);
         }
     }
@@ -373,22 +383,34 @@ __global__ void __launch_bounds__(CartShape<Real, D, K>::THREADS, CartShape<Real
 #pragma unroll
       for (int i = 0; i < 2 * D; ++i)
         f = (i == phi) ? tf[i] : f;
-      Real *fc = U + CS::OFF_FC + 4 * phi;
-      int side = 0;
+      Real a1 = Real(0), a2 = Real(0), a3 = Real(0);
       if (f.x != -2)
         {
           const int fid = f.y & 0x3fffffff;
-          side = (f.y >> 30) & 1;
+          const int side = (f.y >> 30) & 1;
           const int a = phi / 2;
           const Real *fg = prm.face_geo + (long long)fid * (2 * D + 1);
-          fc[0] = __ldg(fg);
-          fc[1] = __ldg(fg + 1 + side * D + a);
-          fc[2] = __ldg(fg + 1 + (1 - side) * D + a);
-          fc[3] = __ldg(prm.penalty + fid);
+          const Real jx = __ldg(fg);
+          const Real jo = __ldg(fg + 1 + side * D + a);
+          const Real tau = __ldg(prm.penalty + fid);
+          if (f.x == -1)
+            {
+              a1 = Real(2) * tau * jx;
+              a2 = -(jo * jx);
+            }
+          else
+            {
+              const Real jb = __ldg(fg + 1 + (1 - side) * D + a);
+              const Real hs = side == 0 ? Real(0.5) : Real(-0.5);
+              a1 = tau * jx;
+              a2 = -(hs * jo * jx);
+              a3 = -(hs * jb * jx);
+            }
         }
-      int *tfs = reinterpret_cast<int *>(U + CS::OFF_TF);
-      tfs[2 * phi] = f.x;
-      tfs[2 * phi + 1] = side;
+      Real *fc = U + CS::OFF_FC + 3 * phi;
+      fc[0] = a1;
+      fc[1] = a2;
+      fc[2] = a3;
     }
   for (int a = p; a < D; a += P)
     {
@@ -409,10 +431,10 @@ __global__ void __launch_bounds__(CartShape<Real, D, K>::THREADS, CartShape<Real
   cstore<Real, D, K, D - 1>(Cf, p, t);
   if constexpr (STAGE)
     {
-      cart_nb_staged<Real, D, K, 0, GLN>(xin[0] ? U - CS::SM_CELL : Af, xin[1] ? U + CS::SM_CELL : Bf, p0,
-                                         nu[0], nd[0]);
-      if constexpr (D == 3)
-        cart_nb_staged<Real, D, K, 1, GLN>(Cf + FS, Cf + 2 * FS, p1, nu[1], nd[1]);
+      cart_nb_staged<Real, D, K, 0, GLN, HERM>(xin[0] ? U - CS::SM_CELL : Af, xin[1] ? U + CS::SM_CELL : Bf, p0,
+                                               sp0, nu[0], nd[0]);
+      // (the y-neighbours' fields are not reused: their scalars are taken in
+      // the y-phase, which keeps four values out of the registers until then)
     }
   cload<Real, D, K, 0>(U, p0, x);
   cart_line<Real, D, K, 0, GLN>(U, x, nu[0], nd[0], t); // t_x, kept in registers
@@ -424,6 +446,8 @@ __global__ void __launch_bounds__(CartShape<Real, D, K>::THREADS, CartShape<Real
       apply_M1<Real, K>(x, t);
       cstore<Real, D, K, 0>(Cf, p0, t); // M_x t_z
       __syncthreads();
+      if constexpr (STAGE)
+        cart_nb_staged<Real, D, K, 1, GLN, HERM>(Cf + FS, Cf + 2 * FS, p1, sp1, nu[1], nd[1]);
       cload<Real, D, K, 1>(U, p1, x);
       cart_line<Real, D, K, 1, GLN>(U, x, nu[1], nd[1], t);
       cstore<Real, D, K, 1>(Bf, p1, t); // t_y
