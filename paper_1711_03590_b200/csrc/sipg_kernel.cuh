@@ -336,10 +336,17 @@ struct KernelShape
   // CART cells are smaller: four CTAs per SM (4 x 55 KB)
   static constexpr int SMEM_CAP = (CART ? 55 : 74) * 1024 / 8;
   static constexpr int NC_SMEM = SMEM_CAP / SM_CELL > 0 ? SMEM_CAP / SM_CELL : 1;
+#ifdef DGX_SP_NC // kernel experiments: cells per CTA / CTAs per SM of the single-pencil kernels
+  static constexpr int NC = DGX_SP_NC;
+#else
   static constexpr int NC = NC_THREADS < NC_SMEM ? NC_THREADS : NC_SMEM;
+#endif
   static constexpr int THREADS = NC * P;
   static constexpr int SMEM_REALS = NC * SM_CELL;
   static constexpr int MIN_BLOCKS =
+#ifdef DGX_SP_MINB
+    DGX_SP_MINB > 0 ? DGX_SP_MINB :
+#endif
     (D == 2 && K >= 7) ? 2
                        : ((CART && 65536 / (THREADS * 4) >= 96 && 4 * SMEM_REALS * 8 + 4096 <= 228 * 1024)
                             ? 4
