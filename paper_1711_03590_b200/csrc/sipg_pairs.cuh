@@ -123,16 +123,19 @@ struct PL
   static constexpr int BRICK = (DGX_PAIRS_BRICK == 1 || (DGX_PAIRS_BRICK > 1 && DGX_PAIRS_BRICK * SM_CELL * 8 <= 113 * 1024))
                                  ? DGX_PAIRS_BRICK : 0;
 #endif
+  // k = 4: 8 threads per cell; 4 cells = one warp per CTA (barriers are free)
+  // and 8 CTAs per SM -- sweep p = 3 (117^3): 10 cells x 3 CTAs 4.68 ms,
+  // 16 x 2 4.99, 8 x 4 4.52, 4 x 8 4.36
 #ifdef DGX_PAIRS_NC
   static constexpr int NC = DGX_PAIRS_NC;
 #else
-  static constexpr int NC = BRICK > 1 ? BRICK : (NC_THREADS < NC_SMEM ? NC_THREADS : NC_SMEM);
+  static constexpr int NC = BRICK > 1 ? BRICK : (K == 4 ? 4 : (NC_THREADS < NC_SMEM ? NC_THREADS : NC_SMEM));
 #endif
   static constexpr int THREADS = NC * G;
 #ifdef DGX_PAIRS_MINB
   static constexpr int MINB = DGX_PAIRS_MINB;
 #else
-  static constexpr int MINB = (220 * 1024) / (NC * SM_CELL * 8 + 1024) >= 3 ? 3 : 2; // CTAs per SM
+  static constexpr int MINB = (K == 4 && !(BRICK > 1)) ? 8 : (220 * 1024) / (NC * SM_CELL * 8 + 1024) >= 3 ? 3 : 2; // CTAs per SM
 #endif
   static constexpr int SMEM_REALS = NC * SM_CELL;
 };
