@@ -82,7 +82,11 @@ struct CartShape
   // cell stride = P mod #banks (3D): the bank run continues across cells
   static constexpr int SM_CELL = D == 3 ? SM_MIN + ((P % NBANK) - (SM_MIN % NBANK) + NBANK) % NBANK
                                         : (SM_MIN + 1) / 2 * 2;
+#ifdef DGX_CART_NC // kernel experiments
+  static constexpr int NC = DGX_CART_NC;
+#else
   static constexpr int NC = (192 / P) > 0 ? 192 / P : 1;
+#endif
   static constexpr int THREADS = NC * P;
   static constexpr int SMEM_REALS = NC * SM_CELL;
   // registers: two lines of K values and the neighbour scalars (measured at

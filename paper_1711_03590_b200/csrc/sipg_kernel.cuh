@@ -336,15 +336,17 @@ struct KernelShape
   // CART cells are smaller: four CTAs per SM (4 x 55 KB)
   static constexpr int SMEM_CAP = (CART ? 55 : 74) * 1024 / 8;
   static constexpr int NC_SMEM = SMEM_CAP / SM_CELL > 0 ? SMEM_CAP / SM_CELL : 1;
-  // 3D, k = 5 (C3): 5 cells = 125 threads fill four warps (7 cells leave 17
-  // of 192 lanes idle) and four CTAs fit an SM; measured on C3: 7 cells x 3 CTAs
-  // 1.768 ms, 6 x 4 1.707, 5 x 5 1.711, 5 x 4 1.691, 4 x 6 1.824 (Hermite-like
-  // basis: 1.708 -> 1.628 ms)
+  // 3D, k = 5 (C3): one cell = 25 threads = one warp per CTA. The barriers of a
+  // one-warp CTA cost nothing, which outweighs the 7 idle lanes: measured on C3,
+  // 7 cells x 3 CTAs/SM 1.768 ms, 6 x 4 1.707, 5 x 4 1.691, 4 x 6 1.824,
+  // 1 x 16 1.608, 1 x 20 1.552, 1 x 22 1.545, 1 x 24 1.548 (Hermite-like basis alike).
+  // k = 7 (two warps per cell) and k = 9 lose with one cell per CTA (5.15 vs 5.06,
+  // 5.18 vs 4.91 ms on the sweep meshes).
   static constexpr bool K5 = APPLY && !CART && D == 3 && K == 5;
 #ifdef DGX_SP_NC // kernel experiments: cells per CTA / CTAs per SM of the single-pencil kernels
   static constexpr int NC = DGX_SP_NC;
 #else
-  static constexpr int NC = K5 ? 5 : (NC_THREADS < NC_SMEM ? NC_THREADS : NC_SMEM);
+  static constexpr int NC = K5 ? 1 : (NC_THREADS < NC_SMEM ? NC_THREADS : NC_SMEM);
 #endif
   static constexpr int THREADS = NC * P;
   static constexpr int SMEM_REALS = NC * SM_CELL;
@@ -352,7 +354,7 @@ struct KernelShape
 #ifdef DGX_SP_MINB
     DGX_SP_MINB > 0 ? DGX_SP_MINB :
 #endif
-    K5 ? 4 :
+    K5 ? 22 :
     (D == 2 && K >= 7) ? 2
                        : ((CART && 65536 / (THREADS * 4) >= 96 && 4 * SMEM_REALS * 8 + 4096 <= 228 * 1024)
                             ? 4

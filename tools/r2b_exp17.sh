@@ -1,7 +1,7 @@
 #!/bin/bash
 mkdir -p gpurun_out
-python -m pytest tests -m gpu -q -x > gpurun_out/x17_pytest.log 2>&1; echo pytest_rc=$?; tail -3 gpurun_out/x17_pytest.log
+python -m pytest tests -m gpu -q -x > gpurun_out/x22_pytest.log 2>&1; echo pytest_rc=$?; tail -3 gpurun_out/x22_pytest.log
 for c in c3 c3h; do
-  timeout 300 python bench.py --config $c --steps 30 --warmup 5 --no-e2e --no-cpu-baseline > gpurun_out/x17_$c.json 2>gpurun_out/x17_$c.err
-  python -c "import json; d=json.load(open('gpurun_out/x17_$c.json')); print('$c', round(d['value']/1e9,2), 'GDoF/s', round(d['ms_per_step'],4), d['roofline']['bound'], round(d['roofline']['frac'],3))"
+  timeout 300 python bench.py --config $c --steps 30 --warmup 5 --no-e2e --no-cpu-baseline > gpurun_out/x22_$c.json 2>gpurun_out/x22_$c.err
+  python -c "import json; d=json.load(open('gpurun_out/x22_$c.json')); print('$c', round(d['value']/1e9,2), 'GDoF/s', round(d['ms_per_step'],4), d['roofline']['bound'], round(d['roofline']['frac'],3))"
 done
