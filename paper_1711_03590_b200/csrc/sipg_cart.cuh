@@ -223,13 +223,29 @@ __device__ __forceinline__ void cart_nb_staged(const Real *F0, const Real *F1, i
 //   rv = A1 (uf - nu) + A2 Df.u + A3 nd,   g jo = A2 (uf - nu)
 //   interior: A1 = tau JxW, A2 = -sgn jo JxW / 2, A3 = -sgn jb JxW / 2
 //   boundary: A1 = 2 tau JxW, A2 = -jo JxW, A3 = 0
-template <typename Real, int D, int K, int A, int S, bool GLN>
+template <typename Real, int D, int K, int A, int S, bool GLN, bool HERM>
 __device__ __forceinline__ void cart_face(const Real *cell, const Real (&u)[K], Real nu, Real nd, Real (&t)[K])
 {
   using T = TabLayout<K>;
   using CS = CartShape<Real, D, K>;
   const Real *fc = cell + CS::OFF_FC + 3 * (2 * A + S);
   const Real a1 = fc[0], a2 = fc[1], a3 = fc[2];
+  if constexpr (HERM)
+    {
+      // Hermite-like: value and derivative at an end point live on the two
+      // dofs next to it (the other entries of Sf, Df are zero)
+      constexpr int me = S == 0 ? 0 : K - 1, mi = S == 0 ? 1 : K - 2;
+      const Real se = tab<Real, K>(T::oSf + S * K + me), si = tab<Real, K>(T::oSf + S * K + mi);
+      const Real de = tab<Real, K>(T::oDf + S * K + me), di = tab<Real, K>(T::oDf + S * K + mi);
+      const Real uf = se * u[me] + si * u[mi];
+      const Real dno = de * u[me] + di * u[mi];
+      const Real delta = uf - nu;
+      const Real rv = a1 * delta + a2 * dno + a3 * nd;
+      const Real gj = a2 * delta;
+      t[me] += rv * se + gj * de;
+      t[mi] += rv * si + gj * di;
+      return;
+    }
   const Real uf = GLN ? (S == 0 ? u[0] : u[K - 1]) : dot_row<Real, K, T::oSf + S * K>(u);
   const Real dno = dot_row<Real, K, T::oDf + S * K>(u);
   const Real delta = uf - nu;
@@ -252,7 +268,7 @@ __device__ __forceinline__ void cart_face(const Real *cell, const Real (&u)[K], 
 }
 
 // t = L_A u for one nodal line along axis A of the task's cell
-template <typename Real, int D, int K, int A, bool GLN>
+template <typename Real, int D, int K, int A, bool GLN, bool HERM>
 __device__ __forceinline__ void cart_line(const Real *cell, const Real (&u)[K], const Real (&nu)[2],
                                           const Real (&nd)[2], Real (&t)[K])
 {
@@ -262,15 +278,12 @@ __device__ __forceinline__ void cart_line(const Real *cell, const Real (&u)[K], 
 #pragma unroll
   for (int m = 0; m < K; ++m)
     t[m] *= c;
-  cart_face<Real, D, K, A, 0, GLN>(cell, u, nu[0], nd[0], t);
-  cart_face<Real, D, K, A, 1, GLN>(cell, u, nu[1], nd[1], t);
+  cart_face<Real, D, K, A, 0, GLN, HERM>(cell, u, nu[0], nd[0], t);
+  cart_face<Real, D, K, A, 1, GLN, HERM>(cell, u, nu[1], nd[1], t);
 }
 
 template <typename Real, int D, int K, int BASIS>
-__global__ void __launch_bounds__(CartShape<Real, D, K>::THREADS,
-                                  // Hermite-like: signs, masks and three line numbers more in registers
-                                  (BASIS == 2 && CartShape<Real, D, K>::MINB > 2) ? CartShape<Real, D, K>::MINB - 1
-                                                                                : CartShape<Real, D, K>::MINB)
+__global__ void __launch_bounds__(CartShape<Real, D, K>::THREADS, CartShape<Real, D, K>::MINB)
   sipg_cart_kernel(const ApplyParams<Real> prm)
 {
   using CS = CartShape<Real, D, K>;
@@ -431,7 +444,7 @@ __global__ void __launch_bounds__(CartShape<Real, D, K>::THREADS,
   __syncthreads();
 
   // last axis (line p, in registers since the load)
-  cart_line<Real, D, K, D - 1, GLN>(U, x, nu[D - 1], nd[D - 1], t);
+  cart_line<Real, D, K, D - 1, GLN, HERM>(U, x, nu[D - 1], nd[D - 1], t);
   cstore<Real, D, K, D - 1>(Cf, p, t);
   if constexpr (STAGE)
     {
@@ -441,7 +454,7 @@ __global__ void __launch_bounds__(CartShape<Real, D, K>::THREADS,
       // the y-phase, which keeps four values out of the registers until then)
     }
   cload<Real, D, K, 0>(U, p0, x);
-  cart_line<Real, D, K, 0, GLN>(U, x, nu[0], nd[0], t); // t_x, kept in registers
+  cart_line<Real, D, K, 0, GLN, HERM>(U, x, nu[0], nd[0], t); // t_x, kept in registers
   __syncthreads(); // staging fields free, C complete
   if constexpr (D == 3)
     {
@@ -453,7 +466,7 @@ __global__ void __launch_bounds__(CartShape<Real, D, K>::THREADS,
       if constexpr (STAGE)
         cart_nb_staged<Real, D, K, 1, GLN, HERM>(Cf + FS, Cf + 2 * FS, p1, sp1, nu[1], nd[1]);
       cload<Real, D, K, 1>(U, p1, x);
-      cart_line<Real, D, K, 1, GLN>(U, x, nu[1], nd[1], t);
+      cart_line<Real, D, K, 1, GLN, HERM>(U, x, nu[1], nd[1], t);
       cstore<Real, D, K, 1>(Bf, p1, t); // t_y
       cload<Real, D, K, 1>(Af, p1, x);
       apply_M1<Real, K>(x, t);
