@@ -34,7 +34,8 @@
 //   are read as flat runs (thread t reads elements t + P m); the cells across
 //   the x- and y-faces are staged in shared memory and the thread then reads
 //   its neighbour lines from there (a thread-contiguous x-line read from HBM
-//   costs one sector per lane and request);
+//   costs one sector per lane and request); an x-neighbour that is the CTA's
+//   adjacent task (tasks run along x) is read from that cell's own field;
 // * volume fields have row stride K and a plane stride S2 = K^2 + pad chosen
 //   per K and word size so that the bank residues of the lines along x and
 //   along y are (nearly) evenly spread; a per-axis permutation of the lines
@@ -42,10 +43,12 @@
 //   thread t equal t + beta mod #banks, and a cell stride = P mod #banks
 //   continues that run across the cells of a CTA: consecutive lanes hit
 //   consecutive banks for every axis, whatever the warp alignment.
-// * each neighbour line is reduced at once to the two scalars a face needs.
+// * each neighbour line is reduced at once to the two scalars a face needs,
+//   and the per-face constants to three flux coefficients (cart_face).
 // Hermite-like basis: the sign-flipped tables (mirror-symmetric M1, K1), the
-// sign applied to u and y, two values per neighbour line read directly (only
-// they are shipped for a ghost cell), masked ghost cells.
+// sign applied to u and y; value and derivative at a face live on the two dofs
+// next to it, so traces, lifts and neighbour reads touch two values per line
+// (only those layers are shipped for a ghost cell); masked ghost cells.
 #pragma once
 
 namespace dgx
