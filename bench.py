@@ -393,6 +393,10 @@ def main():
         op.apply(u, y, hooks=hooks, stream=stream)
 
     def barrier():
+        # drain this rank's exchange streams before the process group's own
+        # collective starts: the exchanger's communicator and torch's never
+        # have kernels in flight at the same time
+        torch.cuda.synchronize()
         if ws > 1:
             dist.barrier()
         torch.cuda.synchronize()
