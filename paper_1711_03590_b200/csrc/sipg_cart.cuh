@@ -165,23 +165,25 @@ __device__ __forceinline__ void cart_nb(const ApplyParams<Real> &prm, const int2
           nu[s] = tab<Real, K>(T::oSf + ro + me) * ve + tab<Real, K>(T::oSf + ro + mi) * vi;
           nd[s] = tab<Real, K>(T::oDf + ro + me) * ve + tab<Real, K>(T::oDf + ro + mi) * vi;
         }
-      return;
     }
-  Real xn[2][K];
-#pragma unroll
-  for (int s = 0; s < 2; ++s)
+  else
     {
-      const int nbs = tf[2 * A + s].x;
-      const Real *un = prm.u + (long long)(nbs >= 0 ? nbs : 0) * NQ;
+      Real xn[2][K];
 #pragma unroll
-      for (int m = 0; m < K; ++m)
-        xn[s][m] = nbs >= 0 ? __ldg(un + gidx<D, K, A>(p, m)) : Real(0);
+      for (int s = 0; s < 2; ++s)
+        {
+          const int nbs = tf[2 * A + s].x;
+          const Real *un = prm.u + (long long)(nbs >= 0 ? nbs : 0) * NQ;
+#pragma unroll
+          for (int m = 0; m < K; ++m)
+            xn[s][m] = nbs >= 0 ? __ldg(un + gidx<D, K, A>(p, m)) : Real(0);
+        }
+      // face s = 0 (low side): the neighbour's high end, and vice versa
+      nu[0] = GLN ? xn[0][K - 1] : dot_row<Real, K, T::oSf + K>(xn[0]);
+      nd[0] = dot_row<Real, K, T::oDf + K>(xn[0]);
+      nu[1] = GLN ? xn[1][0] : dot_row<Real, K, T::oSf>(xn[1]);
+      nd[1] = dot_row<Real, K, T::oDf>(xn[1]);
     }
-  // face s = 0 (low side): the neighbour's high end, and vice versa
-  nu[0] = GLN ? xn[0][K - 1] : dot_row<Real, K, T::oSf + K>(xn[0]);
-  nd[0] = dot_row<Real, K, T::oDf + K>(xn[0]);
-  nu[1] = GLN ? xn[1][0] : dot_row<Real, K, T::oSf>(xn[1]);
-  nd[1] = dot_row<Real, K, T::oDf>(xn[1]);
 }
 
 // The same two scalars from neighbour cells staged in shared memory (fields
@@ -205,15 +207,17 @@ __device__ __forceinline__ void cart_nb_staged(const Real *F0, const Real *F1, i
           nu[s] = tab<Real, K>(T::oSf + ro + me) * ve + tab<Real, K>(T::oSf + ro + mi) * vi;
           nd[s] = tab<Real, K>(T::oDf + ro + me) * ve + tab<Real, K>(T::oDf + ro + mi) * vi;
         }
-      return;
     }
-  Real xn[K];
-  cload<Real, D, K, A>(F0, l, xn);
-  nu[0] = GLN ? xn[K - 1] : dot_row<Real, K, T::oSf + K>(xn);
-  nd[0] = dot_row<Real, K, T::oDf + K>(xn);
-  cload<Real, D, K, A>(F1, l, xn);
-  nu[1] = GLN ? xn[0] : dot_row<Real, K, T::oSf>(xn);
-  nd[1] = dot_row<Real, K, T::oDf>(xn);
+  else
+    {
+      Real xn[K];
+      cload<Real, D, K, A>(F0, l, xn);
+      nu[0] = GLN ? xn[K - 1] : dot_row<Real, K, T::oSf + K>(xn);
+      nd[0] = dot_row<Real, K, T::oDf + K>(xn);
+      cload<Real, D, K, A>(F1, l, xn);
+      nu[1] = GLN ? xn[0] : dot_row<Real, K, T::oSf>(xn);
+      nd[1] = dot_row<Real, K, T::oDf>(xn);
+    }
 }
 
 // One face (side S of the line's axis A) of the line operator: adds
@@ -247,26 +251,28 @@ __device__ __forceinline__ void cart_face(const Real *cell, const Real (&u)[K], 
       const Real gj = a2 * delta;
       t[me] += rv * se + gj * de;
       t[mi] += rv * si + gj * di;
-      return;
-    }
-  const Real uf = GLN ? (S == 0 ? u[0] : u[K - 1]) : dot_row<Real, K, T::oSf + S * K>(u);
-  const Real dno = dot_row<Real, K, T::oDf + S * K>(u);
-  const Real delta = uf - nu;
-  const Real rv = a1 * delta + a2 * dno + a3 * nd;
-  const Real gj = a2 * delta;
-  if constexpr (GLN)
-    {
-      // Gauss-Lobatto: Sf rows are exact unit vectors (the end nodes)
-      t[S == 0 ? 0 : K - 1] += rv;
-#pragma unroll
-      for (int m = 0; m < K; ++m)
-        t[m] += gj * tab<Real, K>(T::oDf + S * K + m);
     }
   else
     {
+      const Real uf = GLN ? (S == 0 ? u[0] : u[K - 1]) : dot_row<Real, K, T::oSf + S * K>(u);
+      const Real dno = dot_row<Real, K, T::oDf + S * K>(u);
+      const Real delta = uf - nu;
+      const Real rv = a1 * delta + a2 * dno + a3 * nd;
+      const Real gj = a2 * delta;
+      if constexpr (GLN)
+        {
+          // Gauss-Lobatto: Sf rows are exact unit vectors (the end nodes)
+          t[S == 0 ? 0 : K - 1] += rv;
 #pragma unroll
-      for (int m = 0; m < K; ++m)
-        t[m] += rv * tab<Real, K>(T::oSf + S * K + m) + gj * tab<Real, K>(T::oDf + S * K + m);
+          for (int m = 0; m < K; ++m)
+            t[m] += gj * tab<Real, K>(T::oDf + S * K + m);
+        }
+      else
+        {
+#pragma unroll
+          for (int m = 0; m < K; ++m)
+            t[m] += rv * tab<Real, K>(T::oSf + S * K + m) + gj * tab<Real, K>(T::oDf + S * K + m);
+        }
     }
 }
 
