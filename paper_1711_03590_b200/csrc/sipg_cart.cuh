@@ -20,13 +20,29 @@
 // reference (the k-point Gauss rule is inside M1 and K1), so the results agree
 // to round-off; the sum order differs like in the collocation kernels.
 //
+// The kernel evaluates it as
+//   y = (M1 x M1 x M1) w,   w = sum_a M1^{-1} L_a u   (M1^{-1} along a),
+// with the 1D tables M1^{-1} K1, M1^{-1} Sf^T, M1^{-1} Df^T built on the host
+// (sipg_launch.cuh): the three line results add up point by point in one field
+// and three mass products follow, instead of two mass products per axis.
+// cond(M1) <= 20 for the Gauss-Lobatto basis and <= 5 for the Lagrange-Gauss
+// basis at p <= 10, so the inverse costs a digit at most (tests: <= 1e-12 in
+// fp64, <= 1e-5 in fp32 up to p = 10). The Hermite-like basis (cond(M1) = 1e3
+// at p = 3, 1e6 at p = 10) keeps the direct form: t_a = L_a u with K1 itself
+// and two mass products per axis,
+//   z: t_z -> C;  x: t_x -> A, C <- M_x C;  y: t_y -> B, A <- M_y A,
+//   C <- M_y C;  x: A <- A + M_x B;  z: y = M_z A + C      (17 field passes).
+//
 // P = K^{D-1} threads per cell; a thread holds one nodal line along the
 // current axis in registers; the 1D matrices are mirror-symmetric and applied
-// in even-odd form from the constant bank.
-//   3D:  z: t_z -> C;  x: t_x -> A, C <- M_x C;  y: t_y -> B, A <- M_y A,
-//        C <- M_y C;  x: A <- A + M_x B;  z: y = M_z A + C.
-// 17 shared-memory field passes and 9 1D products per cell, against 59 and 12
-// (+ the face phase) of the collocation kernels.
+// in even-odd form from the constant bank; end-point rows are used for the low
+// end only and mirrored for the high end (fewer constants in flight: ptxas
+// keeps them in uniform registers and spills those first).
+//   3D:  z: C = L~_z u;  x: C += L~_x u;  y: w = C + L~_y u, C = M_y w;
+//        x: C = M_x C;  z: y = M_z C        (L~ = M1^{-1} L)
+// 11 shared-memory field passes and 6 1D products per cell (+ the staging of
+// the neighbour cells), against 59 passes, 12 products and the face phase of
+// the collocation kernels.
 //
 // The kernel is bound by the L1 / shared-memory data pipe (ncu: 91% busy in
 // its first version), so the layout is built around wavefronts:
@@ -141,49 +157,84 @@ __device__ __forceinline__ void apply_M1(const Real (&x)[K], Real (&y)[K])
 // axis A, for both faces of the axis: everything a face needs from the cell
 // across it. Issued for all axes at task start (every global load of the
 // task is in flight at once).
-template <typename Real, int D, int K, int A, bool GLN, bool HERM>
-__device__ __forceinline__ void cart_nb(const ApplyParams<Real> &prm, const int2 (&tf)[2 * D], int p, Real sp,
-                                        Real (&nu)[2], Real (&nd)[2])
+// End-point value and derivative of a nodal line at its low (index 0) and
+// high (index 1) end from the rows of the low end only: the basis is
+// mirror-symmetric, Sf_1[j] = Sf_0[K-1-j] and Df_1[j] = -Df_0[K-1-j] (half the
+// constants in flight).
+template <typename Real, int K, bool GLN, bool HERM>
+__device__ __forceinline__ void cart_ends(const Real (&u)[K], Real (&val)[2], Real (&der)[2])
 {
   using T = TabLayout<K>;
-  constexpr int NQ = ipow_c(K, D);
   if constexpr (HERM)
     {
-      // Hermite-like: only the two layers next to the face carry a value or a
-      // normal derivative there (read_face_dofs, dof_layout.hpp:291-336) --
-      // and only they are shipped for a ghost neighbour
-#pragma unroll
-      for (int s = 0; s < 2; ++s)
-        {
-          const int nbs = tf[2 * A + s].x;
-          const Real *un = prm.u + (long long)(nbs >= 0 ? nbs : 0) * NQ;
-          const int me = s == 0 ? K - 1 : 0, mi = s == 0 ? K - 2 : 1, ro = s == 0 ? K : 0;
-          Real ve = nbs >= 0 ? __ldg(un + gidx<D, K, A>(p, me)) : Real(0);
-          Real vi = nbs >= 0 ? __ldg(un + gidx<D, K, A>(p, mi)) : Real(0);
-          ve *= sp * hsign<Real, K>(me);
-          vi *= sp * hsign<Real, K>(mi);
-          nu[s] = tab<Real, K>(T::oSf + ro + me) * ve + tab<Real, K>(T::oSf + ro + mi) * vi;
-          nd[s] = tab<Real, K>(T::oDf + ro + me) * ve + tab<Real, K>(T::oDf + ro + mi) * vi;
-        }
+      // Hermite-like: value and derivative at an end point live on the two
+      // dofs next to it (the other entries of Sf, Df are zero)
+      const Real s0 = tab<Real, K>(T::oSf), s1 = tab<Real, K>(T::oSf + 1);
+      const Real d0 = tab<Real, K>(T::oDf), d1 = tab<Real, K>(T::oDf + 1);
+      val[0] = s0 * u[0] + s1 * u[1];
+      val[1] = s0 * u[K - 1] + s1 * u[K - 2];
+      der[0] = d0 * u[0] + d1 * u[1];
+      der[1] = -(d0 * u[K - 1] + d1 * u[K - 2]);
     }
   else
     {
-      Real xn[2][K];
+      Real a = Real(0), b = Real(0), c = Real(0), d = Real(0);
 #pragma unroll
-      for (int s = 0; s < 2; ++s)
+      for (int m = 0; m < K; ++m)
         {
-          const int nbs = tf[2 * A + s].x;
-          const Real *un = prm.u + (long long)(nbs >= 0 ? nbs : 0) * NQ;
-#pragma unroll
-          for (int m = 0; m < K; ++m)
-            xn[s][m] = nbs >= 0 ? __ldg(un + gidx<D, K, A>(p, m)) : Real(0);
+          const Real df = tab<Real, K>(T::oDf + m);
+          c += df * u[m];
+          d += df * u[K - 1 - m];
+          if constexpr (!GLN)
+            {
+              const Real sf = tab<Real, K>(T::oSf + m);
+              a += sf * u[m];
+              b += sf * u[K - 1 - m];
+            }
         }
-      // face s = 0 (low side): the neighbour's high end, and vice versa
-      nu[0] = GLN ? xn[0][K - 1] : dot_row<Real, K, T::oSf + K>(xn[0]);
-      nd[0] = dot_row<Real, K, T::oDf + K>(xn[0]);
-      nu[1] = GLN ? xn[1][0] : dot_row<Real, K, T::oSf>(xn[1]);
-      nd[1] = dot_row<Real, K, T::oDf>(xn[1]);
+      // Gauss-Lobatto: Sf rows are exact unit vectors (the end nodes)
+      val[0] = GLN ? u[0] : a;
+      val[1] = GLN ? u[K - 1] : b;
+      der[0] = c;
+      der[1] = -d;
     }
+}
+
+// The neighbours' face value and normal derivative on the nodal line l along
+// axis A, for both faces of the axis: everything a face needs from the cell
+// across it. Direct global reads (the last axis: coalesced; and every axis
+// when staging is off).
+template <typename Real, int D, int K, int A, bool GLN, bool HERM>
+__device__ __forceinline__ void cart_nb(const ApplyParams<Real> &prm, const int2 (&tf)[2 * D], int l, Real sp,
+                                        Real (&nu)[2], Real (&nd)[2])
+{
+  constexpr int NQ = ipow_c(K, D);
+  Real xn[2][K];
+#pragma unroll
+  for (int s = 0; s < 2; ++s)
+    {
+      const int nbs = tf[2 * A + s].x;
+      const Real *un = prm.u + (long long)(nbs >= 0 ? nbs : 0) * NQ;
+#pragma unroll
+      for (int m = 0; m < K; ++m)
+        {
+          // Hermite-like: only the two layers next to the face carry a value
+          // or a normal derivative there (read_face_dofs, dof_layout.hpp:291-336)
+          // -- and only they are shipped for a ghost neighbour
+          const bool need = !HERM || (s == 0 ? m >= K - 2 : m < 2);
+          xn[s][m] = (need && nbs >= 0) ? __ldg(un + gidx<D, K, A>(l, m)) : Real(0);
+          if constexpr (HERM)
+            xn[s][m] *= sp * hsign<Real, K>(m);
+        }
+    }
+  // face 0 (low side) meets the neighbour's high end, and vice versa
+  Real v[2], d[2];
+  cart_ends<Real, K, GLN, HERM>(xn[0], v, d);
+  nu[0] = v[1];
+  nd[0] = d[1];
+  cart_ends<Real, K, GLN, HERM>(xn[1], v, d);
+  nu[1] = v[0];
+  nd[1] = d[0];
 }
 
 // The same two scalars from neighbour cells staged in shared memory (fields
@@ -193,102 +244,88 @@ template <typename Real, int D, int K, int A, bool GLN, bool HERM>
 __device__ __forceinline__ void cart_nb_staged(const Real *F0, const Real *F1, int l, Real sp, Real (&nu)[2],
                                                Real (&nd)[2])
 {
-  using T = TabLayout<K>;
-  if constexpr (HERM)
-    {
-      // two layers next to the face (the only ones a ghost cell holds)
+  Real xn[2][K];
 #pragma unroll
-      for (int s = 0; s < 2; ++s)
+  for (int s = 0; s < 2; ++s)
+    {
+      const Real *F = s == 0 ? F0 : F1;
+#pragma unroll
+      for (int m = 0; m < K; ++m)
         {
-          const Real *F = s == 0 ? F0 : F1;
-          const int me = s == 0 ? K - 1 : 0, mi = s == 0 ? K - 2 : 1, ro = s == 0 ? K : 0;
-          const Real ve = F[cidx<Real, D, K, A>(l, me)] * (sp * hsign<Real, K>(me));
-          const Real vi = F[cidx<Real, D, K, A>(l, mi)] * (sp * hsign<Real, K>(mi));
-          nu[s] = tab<Real, K>(T::oSf + ro + me) * ve + tab<Real, K>(T::oSf + ro + mi) * vi;
-          nd[s] = tab<Real, K>(T::oDf + ro + me) * ve + tab<Real, K>(T::oDf + ro + mi) * vi;
+          const bool need = !HERM || (s == 0 ? m >= K - 2 : m < 2);
+          xn[s][m] = need ? F[cidx<Real, D, K, A>(l, m)] : Real(0);
+          if constexpr (HERM)
+            xn[s][m] *= sp * hsign<Real, K>(m);
         }
     }
-  else
-    {
-      Real xn[K];
-      cload<Real, D, K, A>(F0, l, xn);
-      nu[0] = GLN ? xn[K - 1] : dot_row<Real, K, T::oSf + K>(xn);
-      nd[0] = dot_row<Real, K, T::oDf + K>(xn);
-      cload<Real, D, K, A>(F1, l, xn);
-      nu[1] = GLN ? xn[0] : dot_row<Real, K, T::oSf>(xn);
-      nd[1] = dot_row<Real, K, T::oDf>(xn);
-    }
+  Real v[2], d[2];
+  cart_ends<Real, K, GLN, HERM>(xn[0], v, d);
+  nu[0] = v[1];
+  nd[0] = d[1];
+  cart_ends<Real, K, GLN, HERM>(xn[1], v, d);
+  nu[1] = v[0];
+  nd[1] = d[0];
 }
 
-// One face (side S of the line's axis A) of the line operator: adds
-// rv Sf_S^T + g jo Df_S^T to t. u: own nodal line; nu, nd: the neighbour's
-// face value and normal derivative (reference coordinates) on the same line
-// (zeros without a neighbour). The per-face constants are folded at task
-// start into three coefficients that cover the interior flux
+// t = M1^{-1} L_A u (Hermite-like basis: L_A u) for one nodal line along axis A
+// of the task's cell: c_A M1^{-1} K1 u plus both faces of the axis. u: own nodal line; nu, nd: the
+// neighbours' face value and normal derivative (reference coordinates) on the
+// same line (zeros without a neighbour). The per-face constants are folded at
+// task start into three coefficients that cover the interior flux
 // (operators.cpp:977-1003), the boundary mirror rule (:1069-1089) and faces not
 // computed on this rank (all zero) without a branch:
 //   rv = A1 (uf - nu) + A2 Df.u + A3 nd,   g jo = A2 (uf - nu)
 //   interior: A1 = tau JxW, A2 = -sgn jo JxW / 2, A3 = -sgn jb JxW / 2
 //   boundary: A1 = 2 tau JxW, A2 = -jo JxW, A3 = 0
-template <typename Real, int D, int K, int A, int S, bool GLN, bool HERM>
-__device__ __forceinline__ void cart_face(const Real *cell, const Real (&u)[K], Real nu, Real nd, Real (&t)[K])
-{
-  using T = TabLayout<K>;
-  using CS = CartShape<Real, D, K>;
-  const Real *fc = cell + CS::OFF_FC + 3 * (2 * A + S);
-  const Real a1 = fc[0], a2 = fc[1], a3 = fc[2];
-  if constexpr (HERM)
-    {
-      // Hermite-like: value and derivative at an end point live on the two
-      // dofs next to it (the other entries of Sf, Df are zero)
-      constexpr int me = S == 0 ? 0 : K - 1, mi = S == 0 ? 1 : K - 2;
-      const Real se = tab<Real, K>(T::oSf + S * K + me), si = tab<Real, K>(T::oSf + S * K + mi);
-      const Real de = tab<Real, K>(T::oDf + S * K + me), di = tab<Real, K>(T::oDf + S * K + mi);
-      const Real uf = se * u[me] + si * u[mi];
-      const Real dno = de * u[me] + di * u[mi];
-      const Real delta = uf - nu;
-      const Real rv = a1 * delta + a2 * dno + a3 * nd;
-      const Real gj = a2 * delta;
-      t[me] += rv * se + gj * de;
-      t[mi] += rv * si + gj * di;
-    }
-  else
-    {
-      const Real uf = GLN ? (S == 0 ? u[0] : u[K - 1]) : dot_row<Real, K, T::oSf + S * K>(u);
-      const Real dno = dot_row<Real, K, T::oDf + S * K>(u);
-      const Real delta = uf - nu;
-      const Real rv = a1 * delta + a2 * dno + a3 * nd;
-      const Real gj = a2 * delta;
-      if constexpr (GLN)
-        {
-          // Gauss-Lobatto: Sf rows are exact unit vectors (the end nodes)
-          t[S == 0 ? 0 : K - 1] += rv;
-#pragma unroll
-          for (int m = 0; m < K; ++m)
-            t[m] += gj * tab<Real, K>(T::oDf + S * K + m);
-        }
-      else
-        {
-#pragma unroll
-          for (int m = 0; m < K; ++m)
-            t[m] += rv * tab<Real, K>(T::oSf + S * K + m) + gj * tab<Real, K>(T::oDf + S * K + m);
-        }
-    }
-}
-
-// t = L_A u for one nodal line along axis A of the task's cell
+// and the result rv Sf^T + g jo Df^T is lifted with M1^{-1} (tables of the low
+// end, mirrored for the high end).
 template <typename Real, int D, int K, int A, bool GLN, bool HERM>
 __device__ __forceinline__ void cart_line(const Real *cell, const Real (&u)[K], const Real (&nu)[2],
                                           const Real (&nd)[2], Real (&t)[K])
 {
   using T = TabLayout<K>;
-  const Real c = cell[CartShape<Real, D, K>::OFF_CC + A];
+  using CS = CartShape<Real, D, K>;
+  const Real c = cell[CS::OFF_CC + A];
   eo_sym<Real, K, T::oK1E, T::oK1O>(u, t);
+  Real uf[2], dno[2], rv[2], gj[2];
+  cart_ends<Real, K, GLN, HERM>(u, uf, dno);
 #pragma unroll
-  for (int m = 0; m < K; ++m)
-    t[m] *= c;
-  cart_face<Real, D, K, A, 0, GLN, HERM>(cell, u, nu[0], nd[0], t);
-  cart_face<Real, D, K, A, 1, GLN, HERM>(cell, u, nu[1], nd[1], t);
+  for (int s = 0; s < 2; ++s)
+    {
+      const Real *fc = cell + CS::OFF_FC + 3 * (2 * A + s);
+      const Real delta = uf[s] - nu[s];
+      rv[s] = fc[0] * delta + fc[1] * dno[s] + fc[2] * nd[s];
+      gj[s] = fc[1] * delta;
+    }
+  if constexpr (HERM)
+    {
+      // Hermite-like (no M1^{-1}: t = L_A u): rv Sf^T + g jo Df^T lives on the
+      // two dofs next to each end
+      const Real s0 = tab<Real, K>(T::oSf), s1 = tab<Real, K>(T::oSf + 1);
+      const Real d0 = tab<Real, K>(T::oDf), d1 = tab<Real, K>(T::oDf + 1);
+#pragma unroll
+      for (int m = 0; m < K; ++m)
+        t[m] *= c;
+      t[0] += rv[0] * s0 + gj[0] * d0;
+      t[1] += rv[0] * s1 + gj[0] * d1;
+      t[K - 1] += rv[1] * s0 - gj[1] * d0;
+      t[K - 2] += rv[1] * s1 - gj[1] * d1;
+    }
+  else
+    {
+#pragma unroll
+      for (int m = 0; m < K; ++m)
+        {
+          const Real ls = tab<Real, K>(T::oLS + m), ld = tab<Real, K>(T::oLD + m);
+          t[m] = c * t[m] + (rv[0] * ls + gj[0] * ld);
+        }
+#pragma unroll
+      for (int m = 0; m < K; ++m)
+        {
+          const Real ls = tab<Real, K>(T::oLS + m), ld = tab<Real, K>(T::oLD + m);
+          t[K - 1 - m] += rv[1] * ls - gj[1] * ld;
+        }
+    }
 }
 
 template <typename Real, int D, int K, int BASIS>
@@ -452,60 +489,112 @@ __global__ void __launch_bounds__(CartShape<Real, D, K>::THREADS, CartShape<Real
     }
   __syncthreads();
 
-  // last axis (line p, in registers since the load)
-  cart_line<Real, D, K, D - 1, GLN, HERM>(U, x, nu[D - 1], nd[D - 1], t);
-  cstore<Real, D, K, D - 1>(Cf, p, t);
-  if constexpr (STAGE)
+  if constexpr (HERM)
     {
-      cart_nb_staged<Real, D, K, 0, GLN, HERM>(xin[0] ? U - CS::SM_CELL : Af, xin[1] ? U + CS::SM_CELL : Bf, p0,
-                                               sp0, nu[0], nd[0]);
-      // (the y-neighbours' fields are not reused: their scalars are taken in
-      // the y-phase, which keeps four values out of the registers until then)
-    }
-  cload<Real, D, K, 0>(U, p0, x);
-  cart_line<Real, D, K, 0, GLN, HERM>(U, x, nu[0], nd[0], t); // t_x, kept in registers
-  __syncthreads(); // staging fields free, C complete
-  if constexpr (D == 3)
-    {
-      cstore<Real, D, K, 0>(Af, p0, t); // t_x
-      cload<Real, D, K, 0>(Cf, p0, x);
-      apply_M1<Real, K>(x, t);
-      cstore<Real, D, K, 0>(Cf, p0, t); // M_x t_z
-      __syncthreads();
+      // y = M_x M_y t_z + M_z (M_y t_x + M_x t_y), t_a = L_a u (two mass products
+      // per axis; no inverse of the ill-conditioned Hermite-like mass matrix)
+      cart_line<Real, D, K, D - 1, GLN, HERM>(U, x, nu[D - 1], nd[D - 1], t);
+      cstore<Real, D, K, D - 1>(Cf, p, t); // t of the last axis
       if constexpr (STAGE)
-        cart_nb_staged<Real, D, K, 1, GLN, HERM>(Cf + FS, Cf + 2 * FS, p1, sp1, nu[1], nd[1]);
-      cload<Real, D, K, 1>(U, p1, x);
-      cart_line<Real, D, K, 1, GLN, HERM>(U, x, nu[1], nd[1], t);
-      cstore<Real, D, K, 1>(Bf, p1, t); // t_y
-      cload<Real, D, K, 1>(Af, p1, x);
-      apply_M1<Real, K>(x, t);
-      cstore<Real, D, K, 1>(Af, p1, t); // M_y t_x
-      cload<Real, D, K, 1>(Cf, p1, x);
-      apply_M1<Real, K>(x, t);
-      cstore<Real, D, K, 1>(Cf, p1, t); // M_y M_x t_z
-      __syncthreads();
-      cload<Real, D, K, 0>(Bf, p0, x);
-      apply_M1<Real, K>(x, t);
-      cload<Real, D, K, 0>(Af, p0, x);
+        cart_nb_staged<Real, D, K, 0, GLN, HERM>(Af, Bf, p0, sp0, nu[0], nd[0]);
+      cload<Real, D, K, 0>(U, p0, x);
+      cart_line<Real, D, K, 0, GLN, HERM>(U, x, nu[0], nd[0], t); // t_x, kept in registers
+      __syncthreads(); // staging fields free, C complete
+      if constexpr (D == 3)
+        {
+          cstore<Real, D, K, 0>(Af, p0, t); // t_x
+          cload<Real, D, K, 0>(Cf, p0, x);
+          apply_M1<Real, K>(x, t);
+          cstore<Real, D, K, 0>(Cf, p0, t); // M_x t_z
+          __syncthreads();
+          if constexpr (STAGE)
+            cart_nb_staged<Real, D, K, 1, GLN, HERM>(Cf + FS, Cf + 2 * FS, p1, sp1, nu[1], nd[1]);
+          cload<Real, D, K, 1>(U, p1, x);
+          cart_line<Real, D, K, 1, GLN, HERM>(U, x, nu[1], nd[1], t);
+          cstore<Real, D, K, 1>(Bf, p1, t); // t_y
+          cload<Real, D, K, 1>(Af, p1, x);
+          apply_M1<Real, K>(x, t);
+          cstore<Real, D, K, 1>(Af, p1, t); // M_y t_x
+          cload<Real, D, K, 1>(Cf, p1, x);
+          apply_M1<Real, K>(x, t);
+          cstore<Real, D, K, 1>(Cf, p1, t); // M_y M_x t_z
+          __syncthreads();
+          cload<Real, D, K, 0>(Bf, p0, x);
+          apply_M1<Real, K>(x, t);
+          cload<Real, D, K, 0>(Af, p0, x);
+#pragma unroll
+          for (int m = 0; m < K; ++m)
+            t[m] += x[m];
+          cstore<Real, D, K, 0>(Af, p0, t); // M_y t_x + M_x t_y
+          __syncthreads();
+          cload<Real, D, K, 2>(Af, p, x);
+          apply_M1<Real, K>(x, t);
+          cload<Real, D, K, 2>(Cf, p, x);
+        }
+      else
+        {
+          cstore<Real, D, K, 0>(Bf, p0, t); // t_x
+          cload<Real, D, K, 0>(Cf, p0, x);
+          apply_M1<Real, K>(x, t);
+          cstore<Real, D, K, 0>(Cf, p0, t); // M_x t_y
+          __syncthreads();
+          cload<Real, D, K, 1>(Bf, p, x);
+          apply_M1<Real, K>(x, t);
+          cload<Real, D, K, 1>(Cf, p, x);
+        }
 #pragma unroll
       for (int m = 0; m < K; ++m)
         t[m] += x[m];
-      cstore<Real, D, K, 0>(Af, p0, t); // M_y t_x + M_x t_y
-      __syncthreads();
-      cload<Real, D, K, 2>(Af, p, x);
-      apply_M1<Real, K>(x, t);
-      cload<Real, D, K, 2>(Cf, p, x);
     }
   else
     {
-      cstore<Real, D, K, 0>(Bf, p0, t); // t_x
+      // last axis (line p, in registers since the load): C = M^{-1} L u along it
+      cart_line<Real, D, K, D - 1, GLN, HERM>(U, x, nu[D - 1], nd[D - 1], t);
+      cstore<Real, D, K, D - 1>(Cf, p, t);
+      if constexpr (STAGE)
+        {
+          cart_nb_staged<Real, D, K, 0, GLN, HERM>(xin[0] ? U - CS::SM_CELL : Af, xin[1] ? U + CS::SM_CELL : Bf, p0,
+                                                   sp0, nu[0], nd[0]);
+          // (the y-neighbours' fields are not reused: their scalars are taken in
+          // the y-phase, which keeps four values out of the registers until then)
+        }
+      cload<Real, D, K, 0>(U, p0, x);
+      cart_line<Real, D, K, 0, GLN, HERM>(U, x, nu[0], nd[0], t); // along x, kept in registers
+      __syncthreads(); // C complete
       cload<Real, D, K, 0>(Cf, p0, x);
-      apply_M1<Real, K>(x, t);
-      cstore<Real, D, K, 0>(Cf, p0, t); // M_x t_y
-      __syncthreads();
-      cload<Real, D, K, 1>(Bf, p, x);
-      apply_M1<Real, K>(x, t);
-      cload<Real, D, K, 1>(Cf, p, x);
+#pragma unroll
+      for (int m = 0; m < K; ++m)
+        t[m] += x[m];
+      if constexpr (D == 3)
+        {
+          cstore<Real, D, K, 0>(Cf, p0, t); // sum over z and x
+          __syncthreads();
+          if constexpr (STAGE)
+            cart_nb_staged<Real, D, K, 1, GLN, HERM>(Cf + FS, Cf + 2 * FS, p1, sp1, nu[1], nd[1]);
+          cload<Real, D, K, 1>(U, p1, x);
+          cart_line<Real, D, K, 1, GLN, HERM>(U, x, nu[1], nd[1], t);
+          cload<Real, D, K, 1>(Cf, p1, x);
+#pragma unroll
+          for (int m = 0; m < K; ++m)
+            x[m] += t[m]; // w = sum_a M_a^{-1} L_a u on this y-line
+          apply_M1<Real, K>(x, t);
+          cstore<Real, D, K, 1>(Cf, p1, t); // M_y w
+          __syncthreads();
+          cload<Real, D, K, 0>(Cf, p0, x);
+          apply_M1<Real, K>(x, t);
+          cstore<Real, D, K, 0>(Cf, p0, t); // M_x M_y w
+          __syncthreads();
+          cload<Real, D, K, 2>(Cf, p, x);
+          apply_M1<Real, K>(x, t); // y = M_z M_x M_y w
+        }
+      else
+        {
+          apply_M1<Real, K>(t, x);
+          cstore<Real, D, K, 0>(Cf, p0, x); // M_x w
+          __syncthreads();
+          cload<Real, D, K, 1>(Cf, p, x);
+          apply_M1<Real, K>(x, t); // y = M_y M_x w
+        }
     }
   if (active)
     {
@@ -513,7 +602,7 @@ __global__ void __launch_bounds__(CartShape<Real, D, K>::THREADS, CartShape<Real
 #pragma unroll
       for (int m = 0; m < K; ++m)
         {
-          Real v = t[m] + x[m];
+          Real v = t[m];
           if constexpr (HERM)
             v = ((gmask >> m) & 1u) ? v * (sp * hsign<Real, K>(m)) : Real(0);
           __stcs(yc + p + P * m, v); // y is not read again (streaming)

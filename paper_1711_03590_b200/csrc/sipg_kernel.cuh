@@ -60,14 +60,18 @@ struct TabLayout
   static constexpr int oDnE = oRD + 2 * K;   // even-odd halves of the nodal D
   static constexpr int oDnO = oDnE + CE * CE;
   static constexpr int oDn = oDnO + CE * CE; // plain nodal D, K x K (Gauss point, node)
-  // 1D mass M1 = S^T W S and stiffness K1 = D^T W D of the nodal basis with the
-  // k-point Gauss rule (even-odd halves): the tensor-product Cartesian kernel
+  // the tensor-product Cartesian kernel (sipg_cart.cuh): 1D mass M1 = S^T W S
+  // of the k-point Gauss rule, and the line operator premultiplied by its
+  // inverse: M1^{-1} K1 with the stiffness K1 = D^T W D (both mirror-symmetric,
+  // even-odd halves), M1^{-1} Sf_s^T and M1^{-1} Df_s^T (the face lifts)
   static constexpr int oM1E = oDn + K * K, oM1O = oM1E + CE * CE;
   static constexpr int oK1E = oM1O + CE * CE, oK1O = oK1E + CE * CE;
-  static constexpr int size = oK1O + CE * CE;
+  static constexpr int oLS = oK1O + CE * CE; // [2][K]
+  static constexpr int oLD = oLS + 2 * K;    // [2][K]
+  static constexpr int size = oLD + 2 * K;
 };
 
-constexpr int tab_size(int K) { return 14 * ((K + 1) / 2) * ((K + 1) / 2) + 3 * K * K + 9 * K; }
+constexpr int tab_size(int K) { return 14 * ((K + 1) / 2) * ((K + 1) / 2) + 3 * K * K + 13 * K; }
 // offset of the table for K (K >= 2) inside the per-precision constant block
 constexpr int tab_offset(int K) { return K <= 2 ? 0 : tab_offset(K - 1) + tab_size(K - 1); }
 constexpr int kMaxK = 11;

@@ -13,6 +13,7 @@
 #include "sipg_adv.cuh"
 
 #include <algorithm>
+#include <cmath>
 #include <mutex>
 #include <vector>
 #include <set>
@@ -111,7 +112,69 @@ std::vector<double> build_table(int K)
         }
   eo_halves(M1, K, o, o + c2);
   o += 2 * c2;
+  // M1^{-1} [K1 | Sf_0^T Sf_1^T Df_0^T Df_1^T]: Gaussian elimination with
+  // partial pivoting on the augmented system (M1 is s.p.d., k <= 11)
+  const int NR = K + 4;
+  std::vector<double> aug(K * (K + NR), 0.0);
+  for (int i = 0; i < K; ++i)
+    {
+      for (int j = 0; j < K; ++j)
+        {
+          aug[i * (K + NR) + j] = M1[i * K + j];
+          aug[i * (K + NR) + K + j] = K1[i * K + j];
+        }
+      for (int s = 0; s < 2; ++s)
+        {
+          aug[i * (K + NR) + 2 * K + s] = t.Sf[s][i];
+          aug[i * (K + NR) + 2 * K + 2 + s] = t.Df[s][i];
+        }
+    }
+  for (int c = 0; c < K; ++c)
+    {
+      int piv = c;
+      for (int r = c + 1; r < K; ++r)
+        if (std::fabs(aug[r * (K + NR) + c]) > std::fabs(aug[piv * (K + NR) + c]))
+          piv = r;
+      if (piv != c)
+        for (int j = 0; j < K + NR; ++j)
+          std::swap(aug[c * (K + NR) + j], aug[piv * (K + NR) + j]);
+      const double d = aug[c * (K + NR) + c];
+      for (int j = 0; j < K + NR; ++j)
+        aug[c * (K + NR) + j] /= d;
+      for (int r = 0; r < K; ++r)
+        if (r != c)
+          {
+            const double f = aug[r * (K + NR) + c];
+            if (f != 0.0)
+              for (int j = 0; j < K + NR; ++j)
+                aug[r * (K + NR) + j] -= f * aug[c * (K + NR) + j];
+          }
+    }
+  std::vector<double> MK(K * K);
+  for (int i = 0; i < K; ++i)
+    for (int j = 0; j < K; ++j)
+      MK[i * K + j] = aug[i * (K + NR) + K + j];
+  // symmetrise the mirror pairs (the even-odd halves assume exact mirror symmetry)
+  for (int i = 0; i < K; ++i)
+    for (int j = 0; j < K; ++j)
+      {
+        const double a = 0.5 * (MK[i * K + j] + MK[(K - 1 - i) * K + (K - 1 - j)]);
+        MK[i * K + j] = MK[(K - 1 - i) * K + (K - 1 - j)] = a;
+      }
+  // Hermite-like basis: cond(M1) grows to 1e6 at p = 10 (the nodal bases stay
+  // below 20), so that kernel keeps K1 itself and two mass products per axis
+#if DGX_BASIS == 2
   eo_halves(K1, K, o, o + c2);
+#else
+  eo_halves(MK, K, o, o + c2);
+#endif
+  o += 2 * c2;
+  for (int s = 0; s < 2; ++s)
+    for (int i = 0; i < K; ++i)
+      {
+        o[s * K + i] = aug[i * (K + NR) + 2 * K + s];           // M1^{-1} Sf_s^T
+        o[2 * K + s * K + i] = aug[i * (K + NR) + 2 * K + 2 + s]; // M1^{-1} Df_s^T
+      }
   return tab;
 }
 
