@@ -12,6 +12,7 @@ not link time. No kernel waits on another (dependencies are stream events and
 copies), so this is safe on one GPU.
 
 usage: python tools/decomposition_overhead.py [n] [p] [R ...] > profiles/r02/decomposition_overhead.txt
+       DGX_DECOMP_CART=1 ... : the C5 shape instead (Cartesian n^3, affine records, tensor-product kernel)
 """
 import os
 import sys
@@ -31,9 +32,12 @@ STEPS = 10
 nq = (p + 1) ** 3
 mesh = D.make_box_mesh(3, [n, n, n], 0.0, False, 1)
 faces = D.enumerate_faces(mesh)
-geo = D.Geometry(source="vertex_bump", vertex_bump_eps=0.1, coefficient="a1")
+CART = bool(os.environ.get("DGX_DECOMP_CART"))
+geo = (D.Geometry(source="mesh") if CART
+       else D.Geometry(source="vertex_bump", vertex_bump_eps=0.1, coefficient="a1"))
 x = D.random_vector(n ** 3 * nq, 3)
-print(f"# C4 shape: deformed {n}^3, p={p}, a(x) folded, fp64, {n ** 3 * nq} DoFs; {STEPS} applies per measurement")
+print((f"# C5 shape: Cartesian {n}^3, p={p}, affine records" if CART else
+       f"# C4 shape: deformed {n}^3, p={p}, a(x) folded") + f", fp64, {n ** 3 * nq} DoFs; {STEPS} applies per measurement")
 base = None
 for R in Rs:
     part = D.partition_cells(mesh, R)
