@@ -1050,7 +1050,9 @@ dgx_stats Operator::stats() const
   long long P = nq_ / k_;
   if (tensor_)
     {
-      st.cells_per_cta = static_cast<int>(192 / P > 0 ? 192 / P : 1); // dev::CartShape
+      st.cells_per_cta = (d_ == 3 && k_ == 7 && precision_ == 0 && basis_ != 2)
+                           ? 4
+                           : static_cast<int>(192 / P > 0 ? 192 / P : 1); // dev::CartShape
       st.cartesian = 2;
     }
   else

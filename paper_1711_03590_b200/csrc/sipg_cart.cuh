@@ -81,7 +81,7 @@ constexpr int cart_pad(int K, int wbytes)
   return (K < 2 || K > 11) ? 0 : (wbytes == 8 ? p8[K - 2] : p4[K - 2]);
 }
 
-template <typename Real, int D, int K>
+template <typename Real, int D, int K, bool HERM = false>
 struct CartShape
 {
   static constexpr int P = ipow_c(K, D - 1);
@@ -104,7 +104,13 @@ struct CartShape
 #ifdef DGX_CART_NC // kernel experiments
   static constexpr int NC = DGX_CART_NC;
 #else
-  static constexpr int NC = (192 / P) > 0 ? 192 / P : 1;
+  // about 192 threads per CTA; 3D k = 7 in fp64 with a nodal basis (C5): 4 cells
+  // (196 threads, 3 CTAs per SM; more x-neighbours inside the CTA): 15.96 ms
+  // against 16.59 (3 cells, 4 CTAs), 19.7 (5 cells, 2 CTAs), 19.1 (6 cells,
+  // 2 CTAs). fp32 (9.97 vs 9.03 ms) and the Hermite-like basis, which does not
+  // share x-neighbours (16.86 vs 16.03 ms), stay at 3 cells.
+  static constexpr int NC =
+    (D == 3 && K == 7 && sizeof(Real) == 8 && !HERM) ? 4 : ((192 / P) > 0 ? 192 / P : 1);
 #endif
   static constexpr int THREADS = NC * P;
   static constexpr int SMEM_REALS = NC * SM_CELL;
@@ -329,12 +335,13 @@ __device__ __forceinline__ void cart_line(const Real *cell, const Real (&u)[K], 
 }
 
 template <typename Real, int D, int K, int BASIS>
-__global__ void __launch_bounds__(CartShape<Real, D, K>::THREADS, CartShape<Real, D, K>::MINB)
+__global__ void __launch_bounds__(CartShape<Real, D, K, BASIS == 2>::THREADS,
+                                  CartShape<Real, D, K, BASIS == 2>::MINB)
   sipg_cart_kernel(const ApplyParams<Real> prm)
 {
-  using CS = CartShape<Real, D, K>;
-  constexpr int P = CS::P, NQ = P * K, FS = CS::FS, NC = CS::NC;
   constexpr bool GLN = BASIS == 0, HERM = BASIS == 2;
+  using CS = CartShape<Real, D, K, HERM>;
+  constexpr int P = CS::P, NQ = P * K, FS = CS::FS, NC = CS::NC;
   // neighbour cells across the x- / y-faces staged in shared memory (the L1
   // data pipe binds in both precisions: C5 fp64 19.8 -> 19.3 ms, fp32 10.8 ->
   // 10.4 ms); the two-value Hermite-like reads go to HBM / L2 directly

@@ -227,7 +227,7 @@ void launch_pairs(const dev::ApplyParams<double> &prm, cudaStream_t s)
 template <typename Real, int D, int K>
 void launch_cart(const dev::ApplyParams<Real> &prm, cudaStream_t s)
 {
-  using CS = dev::CartShape<Real, D, K>;
+  using CS = dev::CartShape<Real, D, K, DGX_BASIS == 2>;
   const size_t smem = (size_t)CS::SMEM_REALS * sizeof(Real);
   auto kern = dev::sipg_cart_kernel<Real, D, K, DGX_BASIS>;
   static std::set<int> configured;
