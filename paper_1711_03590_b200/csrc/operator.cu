@@ -1050,9 +1050,11 @@ dgx_stats Operator::stats() const
   long long P = nq_ / k_;
   if (tensor_)
     {
-      st.cells_per_cta = (d_ == 3 && k_ == 7 && precision_ == 0 && basis_ != 2)
+      // dev::CartShape<Real, D, K, HERM>::NC
+      st.cells_per_cta = d_ == 2 ? static_cast<int>(32 / P > 0 ? 32 / P : 1)
+                         : (k_ == 7 && precision_ == 0 && basis_ != 2)
                            ? 4
-                           : static_cast<int>(192 / P > 0 ? 192 / P : 1); // dev::CartShape
+                           : static_cast<int>(192 / P > 0 ? 192 / P : 1);
       st.cartesian = 2;
     }
   else

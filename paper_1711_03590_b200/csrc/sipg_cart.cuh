@@ -109,8 +109,14 @@ struct CartShape
   // against 16.59 (3 cells, 4 CTAs), 19.7 (5 cells, 2 CTAs), 19.1 (6 cells,
   // 2 CTAs). fp32 (9.97 vs 9.03 ms) and the Hermite-like basis, which does not
   // share x-neighbours (16.86 vs 16.03 ms), stay at 3 cells.
+  // 2D: one warp per CTA (32 / K cells, barriers cost nothing): C2 p = 2 / 5 / 8
+  // 18.3 / 32.9 / 82 us -> 17.0 / 32.8 / 74 us
+#ifndef DGX_CART_2D_WARP
+#define DGX_CART_2D_WARP 1
+#endif
   static constexpr int NC =
-    (D == 3 && K == 7 && sizeof(Real) == 8 && !HERM) ? 4 : ((192 / P) > 0 ? 192 / P : 1);
+    (D == 2 && DGX_CART_2D_WARP) ? (32 / P > 0 ? 32 / P : 1)
+    : (D == 3 && K == 7 && sizeof(Real) == 8 && !HERM) ? 4 : ((192 / P) > 0 ? 192 / P : 1);
 #endif
   static constexpr int THREADS = NC * P;
   static constexpr int SMEM_REALS = NC * SM_CELL;
@@ -124,7 +130,7 @@ struct CartShape
 #ifdef DGX_CART_MINB
   static constexpr int MINB = DGX_CART_MINB;
 #else
-  static constexpr int MINB = MB0 < 1 ? 1 : (MB0 > 6 ? 6 : MB0);
+  static constexpr int MINB = (D == 2 && DGX_CART_2D_WARP) ? 16 : (MB0 < 1 ? 1 : (MB0 > 6 ? 6 : MB0));
 #endif
 };
 
