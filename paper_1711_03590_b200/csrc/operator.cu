@@ -1052,7 +1052,7 @@ dgx_stats Operator::stats() const
     {
       // dev::CartShape<Real, D, K, HERM>::NC
       st.cells_per_cta = d_ == 2 ? static_cast<int>(32 / P > 0 ? 32 / P : 1)
-                         : (k_ == 7 && precision_ == 0 && basis_ != 2)
+                         : ((k_ == 7 && precision_ == 0 && basis_ != 2) || k_ == 4)
                            ? 4
                            : static_cast<int>(192 / P > 0 ? 192 / P : 1);
       st.cartesian = 2;
