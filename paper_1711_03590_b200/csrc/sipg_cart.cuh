@@ -258,20 +258,23 @@ __device__ __forceinline__ void cart_nb(const ApplyParams<Real> &prm, const int2
 // Hermite-like sign of the line)
 template <typename Real, int D, int K, int A, bool GLN, bool HERM>
 __device__ __forceinline__ void cart_nb_staged(const Real *F0, const Real *F1, int l, Real sp, Real (&nu)[2],
-                                               Real (&nd)[2])
+                                               Real (&nd)[2], bool own0 = false, bool own1 = false)
 {
+  // own0 / own1: the field is a CTA partner's own U, which holds the
+  // sign-flipped Hermite-like coefficients already
   Real xn[2][K];
 #pragma unroll
   for (int s = 0; s < 2; ++s)
     {
       const Real *F = s == 0 ? F0 : F1;
+      const bool own = s == 0 ? own0 : own1;
 #pragma unroll
       for (int m = 0; m < K; ++m)
         {
           const bool need = !HERM || (s == 0 ? m >= K - 2 : m < 2);
           xn[s][m] = need ? F[cidx<Real, D, K, A>(l, m)] : Real(0);
           if constexpr (HERM)
-            xn[s][m] *= sp * hsign<Real, K>(m);
+            xn[s][m] *= own ? Real(1) : sp * hsign<Real, K>(m);
         }
     }
   Real v[2], d[2];
@@ -419,14 +422,15 @@ __global__ void __launch_bounds__(CartShape<Real, D, K, BASIS == 2>::THREADS,
           x[m] = ((gmask >> m) & 1u) ? x[m] * (sp * hsign<Real, K>(m)) : Real(0);
       }
   }
-  // x-neighbours that are the CTA's previous / next task (nodal bases: the
-  // Hermite-like U holds sign-flipped, masked values)
+  // x-neighbours that are the CTA's previous / next task (Hermite-like: owned
+  // cells only -- a ghost cell's U is masked to the shipped layers)
   bool xin[2] = {false, false};
-  if constexpr (STAGE && !HERM)
+  if constexpr (STAGE)
     {
-      xin[0] = active && lc > 0 && tf[0].x >= 0 && tf[0].x == __ldg(prm.task_slot + task - 1);
+      xin[0] = active && lc > 0 && tf[0].x >= 0 && tf[0].x == __ldg(prm.task_slot + task - 1) &&
+               (!HERM || tf[0].x < prm.n_owned);
       xin[1] = active && lc + 1 < NC && task + 1 < prm.n_tasks && tf[1].x >= 0 &&
-               tf[1].x == __ldg(prm.task_slot + task + 1);
+               tf[1].x == __ldg(prm.task_slot + task + 1) && (!HERM || tf[1].x < prm.n_owned);
     }
   Real nu[D][2], nd[D][2];
   cart_nb<Real, D, K, D - 1, GLN, HERM>(prm, tf, p, sp, nu[D - 1], nd[D - 1]);
@@ -513,7 +517,8 @@ __global__ void __launch_bounds__(CartShape<Real, D, K, BASIS == 2>::THREADS,
       cart_line<Real, D, K, D - 1, GLN, HERM>(U, x, nu[D - 1], nd[D - 1], t);
       cstore<Real, D, K, D - 1>(Cf, p, t); // t of the last axis
       if constexpr (STAGE)
-        cart_nb_staged<Real, D, K, 0, GLN, HERM>(Af, Bf, p0, sp0, nu[0], nd[0]);
+        cart_nb_staged<Real, D, K, 0, GLN, HERM>(xin[0] ? U - CS::SM_CELL : Af, xin[1] ? U + CS::SM_CELL : Bf,
+                                                 p0, sp0, nu[0], nd[0], xin[0], xin[1]);
       cload<Real, D, K, 0>(U, p0, x);
       cart_line<Real, D, K, 0, GLN, HERM>(U, x, nu[0], nd[0], t); // t_x, kept in registers
       __syncthreads(); // staging fields free, C complete
